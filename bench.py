@@ -1,0 +1,394 @@
+#!/usr/bin/env python3
+"""LDP Mpixel/s benchmark (BASELINE.json metric) on 1..N B200s.
+
+Workload (default, BASELINE.json configs[4] = "C5"): 65,536 face-like
+640x490 uint8 images (GrayImage 490 x 640), LDP k=3, code map + 7x6 cell
+histograms (cells 81 x 91, per-cell clamp = windowed_features semantics).
+The batch is sharded by image across ranks (one process per GPU); each rank
+generates its shard on device keyed by global image index, so every N sees
+identical bytes. With N > 1 the per-image cell histograms are gathered to
+rank 0 (NCCL) inside the timed step. Total work is fixed -> "strong".
+
+A "step" is one pass of the LDP path over the whole batch. Inputs (20.6 GB)
+far exceed L2 (126 MB), so no L2 flush is needed between steps.
+
+  value   : whole-job Mpixel/s, device-resident inputs, CUDA events, max over ranks
+  e2e     : same metric through the host C-ABI entry point (aldp_ldp_batch_host)
+            from pinned host memory: H2D pixels + kernel + D2H codes + D2H hist
+  roofline: algorithmic bytes (1 B in + 1 B code + 4 B x 42 x 56 hist per image)
+            per launch / average launch time, vs MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline: the reference library (oracle/_ref, unmodified reference
+            sources) on this box's host cores, bounded sample
+
+`--impl reference` times the reference's own CPU implementation (oracle/_ref,
+Accelerated path, all host threads) on a bounded sample per step; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (n_images, rows, cols, k, cell_rows, cell_cols, blobs, generator, seed)
+    "c5": (65536, 490, 640, 3, 81, 91, 20, "faces", 11518),
+    "c2": (1024, 490, 640, 3, 81, 91, 20, "faces", 1810),
+    "c4": (1, 16384, 16384, 3, 64, 64, 200, "faces", 42),
+    "c3": (256, 1024, 1024, 3, 0, 0, 0, "ties", 11518),
+    "c1": (1, 490, 640, 3, 0, 0, 0, "random", 42),
+}
+WORKLOAD_NAMES = {
+    "c5": "C5: 65536 x 640x490 face-like, LDP k=3, code map + 7x6 cell histograms",
+    "c2": "C2: 1024 x 640x490 face-like, LDP k=3, code map + 7x6 cell histograms",
+    "c4": "C4: 16384x16384 face-like (200 blobs), LDP k=3, code map + 64x64 cell histograms",
+    "c3": "C3: 256 x 1024x1024 tie-heavy, LDP k=3, code map + whole-image histograms",
+    "c1": "C1: 640x490 uniform random (make_random), LDP k=3, code map + histogram",
+}
+
+
+def hist_bytes_per_image(rows, cols, k, cr, cc):
+    from math import comb
+    cells = 1 if cr == 0 else (rows // cr) * (cols // cc)
+    return cells * comb(8, k) * 4
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=1)
+        sm = sorted(float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit())
+        mx = [float(r[2]) for r in self.rows if len(r) >= 8 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 8 for i in range(4)
+                          if r[4 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx[0] if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# --------------------------------------------------------------------------
+# CPU-side synthetic input for the reference arm (no GPU code on that path):
+# same recipe as the device generator (gradient + blobs + N(0,6) noise).
+# --------------------------------------------------------------------------
+def numpy_faces(n, rows, cols, blobs, seed):
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    out = np.empty((n, rows, cols), np.uint8)
+    xx, yy = np.meshgrid(np.arange(rows, dtype=np.float32), np.arange(cols, dtype=np.float32),
+                         indexing="ij")
+    for i in range(n):
+        th = rng.uniform(0, 2 * math.pi)
+        lo, hi = rng.uniform(40, 120), rng.uniform(120, 220)
+        cx, cy = math.cos(th), math.sin(th)
+        span = abs(cx) * (rows - 1) + abs(cy) * (cols - 1) + 1e-6
+        t = (cx * xx + cy * yy - min(0, cx * (rows - 1)) - min(0, cy * (cols - 1))) / span
+        v = lo + (hi - lo) * t
+        for _ in range(blobs):
+            bx, by = rng.uniform(0, rows), rng.uniform(0, cols)
+            s, a = rng.uniform(5, 60), rng.uniform(-80, 80)
+            v += a * np.exp(-((xx - bx) ** 2 + (yy - by) ** 2) / (2 * s * s))
+        v += rng.normal(0, 6, size=v.shape)
+        out[i] = np.clip(np.rint(v), 0, 255).astype(np.uint8)
+    return out
+
+
+def run_reference(args, cfg_name):
+    """--impl reference: the reference's CPU implementation (oracle/_ref)."""
+    import numpy as np
+    import oracle
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    n, rows, cols, k, cr, cc, blobs, gen, seed = CONFIGS[cfg_name]
+    threads = os.cpu_count() or 1
+    sample = max(threads * 4, 32) if cfg_name in ("c5", "c2") else 1
+    if gen == "faces":
+        px = numpy_faces(sample, rows, cols, blobs, seed)
+    elif gen == "ties":
+        rng = np.random.default_rng(seed)
+        px = rng.integers(0, 3, size=(sample, rows, cols), dtype=np.uint8)
+    else:
+        px = oracle.ref_make_random(rows, cols, seed)[None]
+    kind = "reference" if oracle.have_ref() else "port"
+    run = (lambda: oracle.ref_batch(px, k=k, cell=(cr, cc), threads=threads)) if kind == "reference" \
+        else (lambda: oracle.batch(px, k=k, cell=(cr, cc), threads=threads))
+    for _ in range(args.warmup):
+        run()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        run()
+    dt = (time.perf_counter() - t0) / args.steps
+    mpx = px.size / dt / 1e6
+    line = {
+        "impl": "reference", "metric": "LDP Mpixel/s (code map + histograms)", "value": round(mpx, 3),
+        "unit": "Mpixel/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic (numpy face-like, same recipe)",
+        "config": {"workload": WORKLOAD_NAMES[cfg_name], "images_per_step": int(px.shape[0]),
+                   "parallelism": f"{threads} host threads over images", "cpu_only": True},
+        "cpu_baseline": {"value": round(mpx, 3), "unit": "Mpixel/s", "cores": threads, "kind": kind,
+                         "sample": f"{px.shape[0]} images of {rows}x{cols} per step, ALDP "
+                                   f"(ResponsePath::Accelerated), code map + histograms"},
+        "e2e": {"value": round(mpx, 3), "unit": "Mpixel/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline(host_px, k, cr, cc):
+    """Reference library on this box's host cores, bounded sample."""
+    import oracle
+    threads = os.cpu_count() or 1
+    kind = "reference" if oracle.have_ref() else "port"
+    fn = oracle.ref_batch if kind == "reference" else oracle.batch
+    res = {}
+    n = host_px.shape[0]
+    for label, path, nthreads, count in (("aldp_all_cores", 1, threads, n), ("ldp_all_cores", 0, threads, n // 2),
+                                         ("aldp_1_thread", 1, 1, max(1, n // threads)),
+                                         ("ldp_1_thread", 0, 1, max(1, n // threads // 2))):
+        sub = host_px[:max(count, 1)]
+        kw = {"path": path} if kind == "reference" else {}
+        t0 = time.perf_counter()
+        fn(sub, k=k, cell=(cr, cc), threads=nthreads, **kw)
+        dt = time.perf_counter() - t0
+        res[label] = round(sub.size / dt / 1e6, 3)
+    return {"value": res["aldp_all_cores"], "unit": "Mpixel/s", "cores": threads, "kind": kind,
+            "sample": f"{n} images of {host_px.shape[1]}x{host_px.shape[2]} (first images of the "
+                      f"batch), ALDP/Accelerated, code map + histograms, {threads} threads",
+            "variants_mpx_s": res}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
+    ap.add_argument("--images", type=int, default=0, help="override batch size (testing)")
+    ap.add_argument("--e2e-images", type=int, default=2048)
+    ap.add_argument("--cpu-images", type=int, default=0, help="0 = auto (~10-30 s of CPU work)")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--kernel", default="auto", choices=["auto", "fast", "generic"])
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    if args.impl == "reference":
+        return run_reference(args, args.config)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_1810_11518_b200 as aldp
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    n, rows, cols, k, cr, cc, blobs, gen, seed = CONFIGS[args.config]
+    if args.images:
+        n = args.images
+    lo, hi = n * rank // world, n * (rank + 1) // world
+    mine = hi - lo
+    pitch = cols  # 640/1024/16384: already 16-byte aligned
+    stream = torch.cuda.Stream(dev)
+    sp = stream.cuda_stream
+
+    # ---- inputs, generated on device by global image index (not timed) ----
+    with torch.cuda.stream(stream):
+        if gen == "faces":
+            px = aldp.gen_faces(mine, rows, cols, blobs=blobs, seed=seed, first_index=lo, pitch=pitch,
+                                device=dev, stream=sp)
+        elif gen == "ties":
+            px = aldp.gen_ties(mine, rows, cols, seed=seed, first_index=lo, pitch=pitch, device=dev,
+                               stream=sp)
+        else:
+            import oracle
+            px = torch.from_numpy(oracle.make_random(rows, cols, seed)[None].copy()).to(dev)
+        cells = aldp.grid_cells(rows, cols, cr, cc)
+        nb = aldp.n_bins(k)
+        codes = torch.empty((mine, rows, pitch), dtype=torch.uint8, device=dev)
+        hist = torch.empty((mine, cells, nb), dtype=torch.int32, device=dev)
+        gathered = None
+        if world > 1:
+            # uint16 on the wire: a cell count is at most 81*91 = 7371 < 65536
+            per = [(n * (r + 1) // world - n * r // world) for r in range(world)]
+            assert len(set(per)) == 1, "image count must divide evenly across ranks"
+            wire = torch.empty((mine, cells, nb), dtype=torch.int16, device=dev)
+            if rank == 0:
+                gathered = [torch.empty_like(wire) for _ in range(world)]
+    stream.synchronize()
+
+    def step():
+        aldp.ldp_batch(px, rows, cols, k=k, cell=(cr, cc), codes=codes, hist=hist,
+                       kernel=args.kernel, stream=sp)
+        if world > 1:
+            with torch.cuda.stream(stream):
+                wire.copy_(hist)  # u32 -> u16 (exact, see above)
+                dist.gather(wire, gathered if rank == 0 else None, dst=0)
+
+    # ---- warmup ----
+    for _ in range(args.warmup):
+        step()
+    stream.synchronize()
+
+    # ---- timed region: K steps, events on the launching stream ----
+    sampler = ClockSampler(local) if True else None
+    sampler.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for i in range(args.steps):
+        ev[2 * i].record(stream)
+        aldp.ldp_batch(px, rows, cols, k=k, cell=(cr, cc), codes=codes, hist=hist,
+                       kernel=args.kernel, stream=sp)
+        ev[2 * i + 1].record(stream)
+        if world > 1:
+            with torch.cuda.stream(stream):
+                wire.copy_(hist)
+                dist.gather(wire, gathered if rank == 0 else None, dst=0)
+    t_end.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    total_ms = t_start.elapsed_time(t_end)
+    launch_ms = sum(ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(args.steps)) / args.steps
+    if world > 1:
+        t = torch.tensor([total_ms, launch_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, launch_ms = float(t[0]), float(t[1])
+    ms_per_step = total_ms / args.steps
+    pixels = n * rows * cols
+    value = pixels / (ms_per_step * 1e-3) / 1e6
+
+    # ---- roofline of the dominant kernel (one launch = this rank's shard) ----
+    hbm, peak_src = measured_peaks()
+    bpp_hist = hist_bytes_per_image(rows, cols, k, cr, cc) / (rows * cols)
+    alg_bytes = mine * rows * cols * (2.0 + bpp_hist)
+    achieved = alg_bytes / (launch_ms * 1e-3) / 1e9
+
+    line = {
+        "metric": "LDP Mpixel/s (code map + histograms)", "value": round(value, 1), "unit": "Mpixel/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (device generator, seeded, keyed by global image index)",
+        "config": {"workload": WORKLOAD_NAMES[args.config], "images": n, "rows": rows, "cols": cols,
+                   "k": k, "cell": [cr, cc], "parallelism": f"image shards x{world}",
+                   "l2": "inputs larger than L2 (no flush)" if n * rows * cols > 4 * 126e6 else
+                         "inputs smaller than L2: repeated steps hit L2",
+                   "kernel": args.kernel},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                     "frac": round(achieved / hbm, 4), "traffic": None,
+                     "peak_source": peak_src,
+                     "bytes_per_pixel": round(2.0 + bpp_hist, 4),
+                     "launch_ms": round(launch_ms, 4)},
+        "clocks": clocks,
+        "gpu_launches": args.steps,
+    }
+
+    # ---- end to end through the host C-ABI (pinned host buffers) ----
+    if not args.no_e2e and rank == 0 and world == 1:
+        import ctypes
+        e2n = min(args.e2e_images, mine)
+        hp = torch.empty((e2n, rows, cols), dtype=torch.uint8).pin_memory()
+        hp.copy_(px[:e2n, :, :cols])
+        hc = torch.empty_like(hp).pin_memory()
+        hh = torch.empty((e2n, cells, nb), dtype=torch.int32).pin_memory()
+
+        def e2e_call():
+            st = aldp.lib.aldp_ldp_batch_host(hp.data_ptr(), e2n, rows, cols, k, cr, cc, hc.data_ptr(),
+                                              hh.data_ptr(), None)
+            aldp._check(st)
+
+        for _ in range(args.warmup):
+            e2e_call()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_call()
+        e2e_dt = (time.perf_counter() - t0) / args.steps
+        line["e2e"] = {"value": round(e2n * rows * cols / e2e_dt / 1e6, 1), "unit": "Mpixel/s",
+                       "h2d_bytes_per_step": int(hp.numel()),
+                       "d2h_bytes_per_step": int(hc.numel() + hh.numel() * 4),
+                       "images_per_step": e2n, "api": "aldp_ldp_batch_host (C-ABI, host buffers)"}
+        ok = np.array_equal(hc.numpy(), codes[:e2n, :, :cols].cpu().numpy()) and \
+            np.array_equal(hh.numpy(), hist[:e2n].cpu().numpy())
+        line["e2e"]["matches_device_path"] = bool(ok)
+
+    # ---- CPU baseline (reference library on this box's host cores) ----
+    if not args.no_cpu and rank == 0 and world == 1:
+        cpu_n = args.cpu_images or (min(mine, 4 * (os.cpu_count() or 1) * 8) if rows * cols < 1e6 else 1)
+        host = px[:cpu_n, :, :cols].cpu().numpy()
+        if rows * cols >= 1e8:  # C4: a bounded row band of the big frame
+            host = host[:, :2048, :]
+        line["cpu_baseline"] = cpu_baseline(host, k, cr if rows * cols < 1e8 else cr,
+                                            cc if rows * cols < 1e8 else cc)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

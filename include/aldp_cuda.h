@@ -1,0 +1,152 @@
+/*
+ * aldp_cuda.h -- C-ABI of the B200 LDP path (libaldp_b200.so).
+ *
+ * Plain C: pointers, sizes and status codes; no C++ or torch types cross this
+ * boundary. The C++ drop-in (include/aldp/*.hpp, namespace aldp) and the
+ * Python host layer (paper_1810_11518_b200/__init__.py, ctypes) both sit on
+ * top of it. See INTEGRATION.md for the binding a reference maintainer adds.
+ *
+ * Semantics follow the reference exactly (paths relative to the reference
+ * tree):
+ *  - responses: the eight Kirsch compass responses, clamp-to-edge border
+ *    (proj/src/image.cpp:36-40, proj/src/kirsch.cpp:63-157);
+ *  - code: top-k directions by (response desc, index asc), exactly k bits,
+ *    signed responses (proj/src/descriptors.cpp:83-102);
+ *  - bins: rank among the popcount-k codes in ascending code order
+ *    (proj/src/descriptors.cpp:25-45,104-113; the reference defines k == 3
+ *    only, 56 bins -- other k are this library's extension, C(8,k) bins);
+ *  - histograms: every pixel of the image (proj/src/descriptors.cpp:123-139),
+ *    or per cell with each cell clamped as an independent image, floor grid,
+ *    row-major cells (proj/src/windowing.cpp:8-19,35-63; rectangular cells
+ *    are this library's extension of the square `window`).
+ *
+ * Thread safety: every entry point may be called concurrently from several
+ * host threads; device work is ordered on the caller's stream.
+ */
+#ifndef ALDP_CUDA_H
+#define ALDP_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    ALDP_OK = 0,
+    ALDP_EINVAL = 1, /* maps to std::invalid_argument in the C++ layer */
+    ALDP_ERANGE = 2, /* maps to std::out_of_range */
+    ALDP_ECUDA = 3,  /* CUDA runtime failure -> std::runtime_error */
+    ALDP_ENOMEM = 4  /* device/host allocation failure -> std::runtime_error */
+} aldp_status;
+
+/* Response path selector, mirroring aldp::ResponsePath (kirsch.hpp:88) and
+ * the Ldp/Aldp descriptors (descriptors.hpp:13). Both values produce
+ * identical outputs by contract (descriptors.hpp:53-54); both run the same
+ * B200 kernel. */
+enum { ALDP_PATH_NAIVE = 0, ALDP_PATH_ACCELERATED = 1 };
+
+/* One batched launch over device-resident images.
+ *
+ *  d_pixels    n_images images of rows x cols uint8, row pitch `pitch`
+ *              bytes, image stride `img_stride` bytes.
+ *  k           1..7 (the reference's ldp_code range, descriptors.hpp:26).
+ *  cell_rows,  0,0: one whole-image histogram per image (ldp_histogram).
+ *  cell_cols   otherwise a floor grid of cell_rows x cell_cols cells, each
+ *              clamped as an independent image (windowed_features); both
+ *              must be in [3, rows] x [3, cols].
+ *  d_codes     nullable. Code map, whole-image clamp (the per-pixel code of
+ *              descriptors.cpp:129-136), row pitch codes_pitch, image stride
+ *              codes_img_stride.
+ *  d_hist      nullable. uint32 [n_images][grid_cells][aldp_n_bins(k)];
+ *              overwritten (zeroed by the call, stream-ordered).
+ *
+ * Asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream).
+ * No hidden allocation; caller owns every buffer. */
+typedef struct {
+    const uint8_t* d_pixels;
+    int64_t img_stride;
+    int rows, cols, pitch;
+    int n_images;
+    int k;
+    int cell_rows, cell_cols;
+    uint8_t* d_codes;
+    int64_t codes_img_stride;
+    int codes_pitch;
+    uint32_t* d_hist;
+} aldp_ldp_args;
+
+aldp_status aldp_ldp_batch(const aldp_ldp_args* args, void* stream);
+
+/* Kernel selection for aldp_ldp_batch: AUTO picks the packed sm_100a kernel
+ * whenever the layout allows it (cols, pitch and strides multiples of 4,
+ * k != 4) and the generic per-pixel kernel otherwise. FAST fails with
+ * ALDP_EINVAL when the layout does not allow it. Both are CUDA; there is no
+ * CPU path. */
+enum { ALDP_KERNEL_AUTO = 0, ALDP_KERNEL_FAST = 1, ALDP_KERNEL_GENERIC = 2 };
+aldp_status aldp_ldp_batch_ex(const aldp_ldp_args* args, int kernel, void* stream);
+
+/* Number of histogram bins for k: C(8, k) (56 for k == 3), 0 if k invalid. */
+int aldp_n_bins(int k);
+
+/* Number of cells of the floor grid (windowing.cpp:8-19 generalised):
+ * (rows / cell_rows) * (cols / cell_cols); 1 for cell_rows == 0. Returns -1
+ * for invalid geometry (cell < 3 or larger than the image). */
+int64_t aldp_grid_cells(int rows, int cols, int cell_rows, int cell_cols);
+
+/* ---- host-buffer entry points: the reference's public functions ----
+ * These copy host pixels to the device, run aldp_ldp_batch on an internal
+ * per-thread stream, and copy results back. They replace, one for one:   */
+
+/* aldp::ldp_histogram (include/aldp/descriptors.hpp:55). k must be 3
+ * (descriptors.cpp:124-126) -> ALDP_EINVAL otherwise; image >= 3x3. */
+aldp_status aldp_ldp_histogram(const uint8_t* pixels, int rows, int cols, int k, int path,
+                               uint64_t* bins56);
+
+/* aldp::windowed_features for Descriptor::Ldp / ::Aldp
+ * (include/aldp/windowing.hpp:34-36): out is [grid_cells][56] uint64 in
+ * row-major window order; out_len must be >= cells*56. window < 3 or larger
+ * than the image -> ALDP_EINVAL (windowing.cpp:9-17). */
+aldp_status aldp_windowed_features(const uint8_t* pixels, int rows, int cols, int window,
+                                   int path, uint64_t* out, size_t out_len);
+
+/* NEW (the reference has no code-map entry point; this is the code that
+ * descriptors.cpp:129-136 computes per pixel): codes[rows*cols]. */
+aldp_status aldp_ldp_code_map(const uint8_t* pixels, int rows, int cols, int k, int path,
+                              uint8_t* codes);
+
+/* Host batch: n contiguous rows x cols images in host memory (pinned or
+ * pageable) -> optional host code maps and uint32 histograms, one H2D and
+ * D2H per call, device buffers cached per thread. The end-to-end path. */
+aldp_status aldp_ldp_batch_host(const uint8_t* pixels, int n_images, int rows, int cols, int k,
+                                int cell_rows, int cell_cols, uint8_t* codes, uint32_t* hist,
+                                void* stream);
+
+/* Message for the last non-OK status returned on this host thread. */
+const char* aldp_last_error(void);
+
+/* ---- synthetic inputs (device generators, not part of the timed path) ----
+ * Deterministic, keyed by (seed, first_index + i) so any sharding of a batch
+ * sees identical bytes. */
+
+/* Face-like images (BASELINE.json configs 2, 4, 5): linear gradient with a
+ * seeded direction and endpoints, `blobs` Gaussian blobs (sigma U[5,60] px,
+ * amplitude U[-80,80], centres uniform), N(0,6) noise, rounded and clamped. */
+aldp_status aldp_gen_faces(uint8_t* d_out, int n_images, int rows, int cols, int pitch,
+                           int64_t img_stride, int blobs, uint64_t seed, int64_t first_index,
+                           void* stream);
+
+/* Tie-heavy images (config 3): i.i.d. {0,1,2}, then constant rectangles
+ * painted until about half the area is covered. */
+aldp_status aldp_gen_ties(uint8_t* d_out, int n_images, int rows, int cols, int pitch,
+                          int64_t img_stride, uint64_t seed, int64_t first_index, void* stream);
+
+/* Library identity (for load checks): "aldp_b200 <version> sm_100a". */
+const char* aldp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ALDP_CUDA_H */

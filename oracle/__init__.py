@@ -1,0 +1,211 @@
+"""Parity oracles for the LDP path -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline legs may
+import this package; the product package (paper_1810_11518_b200) never does.
+
+Two checkers, both CPU:
+  * ``port``      -- liboracle.so, this repo's plain-C restatement of the
+                     reference algorithm (ldp_oracle.c, each function cites
+                     the reference file:line it follows);
+  * ``reference`` -- _ref/libaldp_ref.so, the UNMODIFIED reference library
+                     compiled from /root/reference/proj/src (Makefile here)
+                     behind an extern "C" shim (ref_shim.cpp). Built in the
+                     dev container; the prebuilt .so travels to the GPU box.
+The port is pinned against the reference's golden fixtures and against the
+reference library itself (tests/test_oracle.py).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+PORT_PATH = os.path.join(_HERE, "liboracle.so")
+REF_PATH = os.path.join(_HERE, "_ref", "libaldp_ref.so")
+
+_P, _I, _I64, _U32 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_uint32
+
+
+def _load_port():
+    L = ctypes.CDLL(PORT_PATH)
+    L.oracle_make_random.argtypes = [_I, _I, _U32, _P]
+    L.oracle_responses.argtypes = [_P, _I, _I, _I, _I, _P]
+    L.oracle_ldp_code.argtypes = [_P, _I]
+    L.oracle_bin_index.argtypes = [_I, _I]
+    L.oracle_n_bins.argtypes = [_I]
+    L.oracle_code_map.argtypes = [_P, _I, _I, _I, _P]
+    L.oracle_histogram.argtypes = [_P, _I, _I, _I, _P]
+    L.oracle_cell_histograms.argtypes = [_P, _I, _I, _I, _I, _I, _P]
+    L.oracle_batch.argtypes = [_P, _I64, _I, _I, _I, _I, _I, _P, _P, _I]
+    return L
+
+
+def _load_ref():
+    L = ctypes.CDLL(REF_PATH)
+    L.ref_make_random.argtypes = [_I, _I, _U32, _P]
+    L.ref_responses.argtypes = [_P, _I, _I, _I, _I, _I, _P]
+    L.ref_ldp_code.argtypes = [_P, _I, _P]
+    L.ref_ldp_bin_index.argtypes = [_I]
+    L.ref_code_map.argtypes = [_P, _I, _I, _I, _I, _P]
+    L.ref_ldp_histogram.argtypes = [_P, _I, _I, _I, _I, _P]
+    L.ref_windowed.argtypes = [_P, _I, _I, _I, _I, _P, _P]
+    L.ref_batch.argtypes = [_P, _I64, _I, _I, _I, _I, _I, _I, _P, _P, _I]
+    L.ref_median_seconds_batch.argtypes = [_P, _I64, _I, _I, _I, _I, _I, _I, _P, _P, _I, _I]
+    L.ref_median_seconds_batch.restype = ctypes.c_double
+    return L
+
+
+_port = None
+_ref = None
+
+
+def port():
+    global _port
+    if _port is None:
+        _port = _load_port()
+    return _port
+
+
+def ref():
+    global _ref
+    if _ref is None:
+        _ref = _load_ref()
+    return _ref
+
+
+def have_ref() -> bool:
+    return os.path.exists(REF_PATH)
+
+
+def _img(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.uint8)
+
+
+# ---- port (C restatement) ----
+def make_random(rows: int, cols: int, seed: int) -> np.ndarray:
+    out = np.empty((rows, cols), np.uint8)
+    port().oracle_make_random(rows, cols, seed, out.ctypes.data)
+    return out
+
+
+def responses(img, x: int, y: int) -> np.ndarray:
+    a = _img(img)
+    out = np.empty(8, np.int32)
+    port().oracle_responses(a.ctypes.data, a.shape[0], a.shape[1], x, y, out.ctypes.data)
+    return out
+
+
+def ldp_code(m, k: int = 3) -> int:
+    v = np.ascontiguousarray(m, dtype=np.int32)
+    return port().oracle_ldp_code(v.ctypes.data, k)
+
+
+def bin_index(code: int, k: int = 3) -> int:
+    return port().oracle_bin_index(code, k)
+
+
+def n_bins(k: int) -> int:
+    return port().oracle_n_bins(k)
+
+
+def code_map(img, k: int = 3) -> np.ndarray:
+    a = _img(img)
+    out = np.empty_like(a)
+    if port().oracle_code_map(a.ctypes.data, a.shape[0], a.shape[1], k, out.ctypes.data):
+        raise ValueError("bad arguments")
+    return out
+
+
+def histogram(img, k: int = 3) -> np.ndarray:
+    a = _img(img)
+    out = np.zeros(n_bins(k), np.uint64)
+    if port().oracle_histogram(a.ctypes.data, a.shape[0], a.shape[1], k, out.ctypes.data):
+        raise ValueError("bad arguments")
+    return out
+
+
+def cell_histograms(img, cell_rows: int, cell_cols: int, k: int = 3) -> np.ndarray:
+    a = _img(img)
+    gr, gc = a.shape[0] // max(cell_rows, 1), a.shape[1] // max(cell_cols, 1)
+    out = np.zeros((max(gr * gc, 1), n_bins(k)), np.uint64)
+    if port().oracle_cell_histograms(a.ctypes.data, a.shape[0], a.shape[1], cell_rows, cell_cols, k,
+                                     out.ctypes.data) < 0:
+        raise ValueError("bad arguments")
+    return out
+
+
+def batch(pixels, k: int = 3, cell=(0, 0), codes: bool = True, hist: bool = True,
+          threads: int = 0):
+    """Batch [n, rows, cols] -> (codes | None, hist uint64 [n, cells, bins] | None)."""
+    px = np.ascontiguousarray(pixels, dtype=np.uint8)
+    if px.ndim == 2:
+        px = px[None]
+    n, rows, cols = px.shape
+    cells = 1 if cell[0] == 0 else (rows // cell[0]) * (cols // cell[1])
+    c = np.empty_like(px) if codes else None
+    h = np.zeros((n, cells, n_bins(k)), np.uint64) if hist else None
+    threads = threads or os.cpu_count() or 1
+    if port().oracle_batch(px.ctypes.data, n, rows, cols, k, cell[0], cell[1],
+                           c.ctypes.data if c is not None else None,
+                           h.ctypes.data if h is not None else None, threads):
+        raise ValueError("bad arguments")
+    return c, h
+
+
+# ---- reference library ----
+def ref_batch(pixels, k: int = 3, cell=(0, 0), codes: bool = True, hist: bool = True,
+              threads: int = 0, path: int = 1):
+    px = np.ascontiguousarray(pixels, dtype=np.uint8)
+    if px.ndim == 2:
+        px = px[None]
+    n, rows, cols = px.shape
+    nb = n_bins(k)
+    cells = 1 if cell[0] == 0 else (rows // cell[0]) * (cols // cell[1])
+    c = np.empty_like(px) if codes else None
+    h = np.zeros((n, cells, nb), np.uint64) if hist else None
+    threads = threads or os.cpu_count() or 1
+    st = ref().ref_batch(px.ctypes.data, n, rows, cols, k, cell[0], cell[1], path,
+                         c.ctypes.data if c is not None else None,
+                         h.ctypes.data if h is not None else None, threads)
+    if st:
+        raise {1: ValueError, 2: IndexError}.get(st, RuntimeError)("reference rejected the call")
+    return c, h
+
+
+def ref_ldp_histogram(img, k: int = 3, path: int = 1) -> np.ndarray:
+    a = _img(img)
+    out = np.zeros(56, np.uint64)
+    st = ref().ref_ldp_histogram(a.ctypes.data, a.shape[0], a.shape[1], k, path, out.ctypes.data)
+    if st:
+        raise {1: ValueError, 2: IndexError}.get(st, RuntimeError)("reference rejected the call")
+    return out
+
+
+def ref_windowed(img, window: int, path: int = 1) -> np.ndarray:
+    a = _img(img)
+    gr, gc = a.shape[0] // window, a.shape[1] // window
+    out = np.zeros((max(gr * gc, 1), 56), np.uint64)
+    n = ctypes.c_int64(0)
+    st = ref().ref_windowed(a.ctypes.data, a.shape[0], a.shape[1], window, path, out.ctypes.data,
+                            ctypes.byref(n))
+    if st:
+        raise {1: ValueError, 2: IndexError}.get(st, RuntimeError)("reference rejected the call")
+    return out[: n.value]
+
+
+def ref_make_random(rows: int, cols: int, seed: int) -> np.ndarray:
+    out = np.empty((rows, cols), np.uint8)
+    if ref().ref_make_random(rows, cols, seed, out.ctypes.data):
+        raise ValueError("bad dimensions")
+    return out
+
+
+def ref_responses(img, x: int, y: int, path: int = 0) -> np.ndarray:
+    a = _img(img)
+    out = np.empty(8, np.int32)
+    st = ref().ref_responses(a.ctypes.data, a.shape[0], a.shape[1], x, y, path, out.ctypes.data)
+    if st:
+        raise {1: ValueError, 2: IndexError}.get(st, RuntimeError)("reference rejected the call")
+    return out

@@ -1,0 +1,274 @@
+/*
+ * ldp_oracle.c -- CPU restatement of the reference's LDP path.
+ *
+ * TEST INFRASTRUCTURE ONLY. This file is the parity checker for the B200
+ * kernels. Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load it; the product path (paper_1810_11518_b200)
+ * never links or calls it.
+ *
+ * Every function restates one reference function (paths relative to the
+ * reference tree, proj/...):
+ *   oracle_make_random      src/image.cpp:75-83      (std::mt19937, low byte)
+ *   oracle_sample           src/image.cpp:36-40      (clamp-to-edge)
+ *   oracle_responses        src/kirsch.cpp:63-84     (naive 3x3 dot products)
+ *                           masks: src/kirsch.cpp:10-29 (ring + base ring)
+ *   oracle_ldp_code         src/descriptors.cpp:83-102 (k selection passes,
+ *                           strict '>' so the lowest direction wins ties)
+ *   oracle_bin_index        src/descriptors.cpp:25-45,104-106 (ascending
+ *                           rank among popcount-k codes; the reference only
+ *                           defines k == 3 -- k != 3 is this repo's extension)
+ *   oracle_code_map         the per-pixel loop of src/descriptors.cpp:129-136
+ *   oracle_histogram        src/descriptors.cpp:123-139
+ *   oracle_cell_histograms  src/windowing.cpp:8-19,35-63 (floor grid, each
+ *                           cell clamped as its own image, row-major cells);
+ *                           rectangular cells are this repo's extension.
+ *
+ * Parity pins: tests/test_oracle.py checks this file against the reference's
+ * golden fixtures (tests/golden/, converted by tests/golden/make_golden.py)
+ * and against the reference library itself compiled into oracle/_ref/.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <pthread.h>
+
+/* Ring positions clockwise from the top-left neighbour (kirsch.cpp:11-12). */
+static const int kRing[8][2] = {{-1, -1}, {-1, 0}, {-1, 1}, {0, 1},
+                                {1, 1},   {1, 0},  {1, -1}, {0, -1}};
+/* Mask 0's ring weights; mask i at ring slot j is kBase[(j + i) % 8]
+ * (kirsch.cpp:15,25). */
+static const int kBase[8] = {-3, -3, 5, 5, 5, -3, -3, -3};
+
+static int g_masks[8][3][3];
+static int g_masks_ready = 0;
+
+static void build_masks(void) {
+    if (g_masks_ready) return;
+    for (int i = 0; i < 8; ++i) {
+        g_masks[i][1][1] = 0;
+        for (int j = 0; j < 8; ++j)
+            g_masks[i][kRing[j][0] + 1][kRing[j][1] + 1] = kBase[(j + i) % 8];
+    }
+    g_masks_ready = 1;
+}
+
+/* ---- std::mt19937 (image.cpp:75-83 uses its low 8 bits per pixel) ---- */
+typedef struct { uint32_t mt[624]; int idx; } mt19937;
+
+static void mt_seed(mt19937* s, uint32_t seed) {
+    s->mt[0] = seed;
+    for (int i = 1; i < 624; ++i)
+        s->mt[i] = 1812433253u * (s->mt[i - 1] ^ (s->mt[i - 1] >> 30)) + (uint32_t)i;
+    s->idx = 624;
+}
+
+static uint32_t mt_next(mt19937* s) {
+    if (s->idx >= 624) {
+        for (int i = 0; i < 624; ++i) {
+            uint32_t y = (s->mt[i] & 0x80000000u) | (s->mt[(i + 1) % 624] & 0x7fffffffu);
+            s->mt[i] = s->mt[(i + 397) % 624] ^ (y >> 1) ^ ((y & 1u) ? 0x9908b0dfu : 0u);
+        }
+        s->idx = 0;
+    }
+    uint32_t y = s->mt[s->idx++];
+    y ^= y >> 11;
+    y ^= (y << 7) & 0x9d2c5680u;
+    y ^= (y << 15) & 0xefc60000u;
+    y ^= y >> 18;
+    return y;
+}
+
+void oracle_make_random(int rows, int cols, uint32_t seed, uint8_t* out) {
+    mt19937 s;
+    mt_seed(&s, seed);
+    const size_t n = (size_t)rows * (size_t)cols;
+    for (size_t i = 0; i < n; ++i) out[i] = (uint8_t)(mt_next(&s) & 0xFFu);
+}
+
+/* ---- sampling / responses ---- */
+static inline int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+/* Clamp-to-edge inside the window [x0, x0+rows) x [y0, y0+cols) of an image
+ * with row pitch `pitch` (image.cpp:36-40; a window is a cropped image,
+ * windowing.cpp:21-33,42). */
+static inline int sample_win(const uint8_t* px, int pitch, int x0, int y0, int rows,
+                             int cols, int x, int y) {
+    const int cx = clampi(x, x0, x0 + rows - 1);
+    const int cy = clampi(y, y0, y0 + cols - 1);
+    return px[(size_t)cx * (size_t)pitch + (size_t)cy];
+}
+
+int oracle_sample(const uint8_t* px, int rows, int cols, int x, int y) {
+    return sample_win(px, cols, 0, 0, rows, cols, x, y);
+}
+
+static void responses_win(const uint8_t* px, int pitch, int x0, int y0, int rows, int cols,
+                          int x, int y, int m[8]) {
+    build_masks();
+    int nb[3][3];
+    for (int k = -1; k <= 1; ++k)
+        for (int l = -1; l <= 1; ++l)
+            nb[k + 1][l + 1] = sample_win(px, pitch, x0, y0, rows, cols, x + k, y + l);
+    for (int i = 0; i < 8; ++i) {
+        int acc = 0;
+        for (int k = 0; k < 3; ++k)
+            for (int l = 0; l < 3; ++l) acc += g_masks[i][k][l] * nb[k][l];
+        m[i] = acc;
+    }
+}
+
+/* kirsch.cpp:63-84: eight signed responses at (x, y), clamped borders. */
+void oracle_responses(const uint8_t* px, int rows, int cols, int x, int y, int32_t* out8) {
+    int m[8];
+    responses_win(px, cols, 0, 0, rows, cols, x, y, m);
+    for (int i = 0; i < 8; ++i) out8[i] = m[i];
+}
+
+/* descriptors.cpp:83-102: k passes, each picks the largest unused response
+ * with strict '>', so ties keep the lowest direction index. Returns -1 for
+ * k outside [1, 7] (the reference throws std::invalid_argument). */
+int oracle_ldp_code(const int32_t* m, int k) {
+    if (k < 1 || k > 7) return -1;
+    int used[8] = {0};
+    unsigned code = 0;
+    for (int picked = 0; picked < k; ++picked) {
+        int best = -1;
+        for (int i = 0; i < 8; ++i)
+            if (!used[i] && (best < 0 || m[i] > m[best])) best = i;
+        used[best] = 1;
+        code |= 1u << best;
+    }
+    return (int)code;
+}
+
+static int popcount8(unsigned c) {
+    int n = 0;
+    for (int b = 0; b < 8; ++b) n += (c >> b) & 1u;
+    return n;
+}
+
+/* descriptors.cpp:25-45,104-106: rank of `code` among the codes with the same
+ * popcount k, ascending by value; -1 if popcount(code) != k. */
+int oracle_bin_index(int code, int k) {
+    if (code < 0 || code > 255 || popcount8((unsigned)code) != k) return -1;
+    int rank = 0;
+    for (int c = 0; c < code; ++c)
+        if (popcount8((unsigned)c) == k) ++rank;
+    return rank;
+}
+
+/* C(8, k): number of bins for popcount-k codes (56 for k = 3). */
+int oracle_n_bins(int k) {
+    if (k < 1 || k > 7) return -1;
+    int n = 0;
+    for (int c = 0; c < 256; ++c) n += popcount8((unsigned)c) == k;
+    return n;
+}
+
+static int code_win(const uint8_t* px, int pitch, int x0, int y0, int rows, int cols, int x,
+                    int y, int k) {
+    int m[8];
+    responses_win(px, pitch, x0, y0, rows, cols, x, y, m);
+    return oracle_ldp_code(m, k);
+}
+
+/* The per-pixel code of descriptors.cpp:129-136 written out as a map:
+ * codes[x * cols + y] = ldp_code(responses(img, x, y), k). Image clamp. */
+int oracle_code_map(const uint8_t* px, int rows, int cols, int k, uint8_t* codes) {
+    if (k < 1 || k > 7 || rows < 3 || cols < 3) return -1;
+    for (int x = 0; x < rows; ++x)
+        for (int y = 0; y < cols; ++y)
+            codes[(size_t)x * cols + y] = (uint8_t)code_win(px, cols, 0, 0, rows, cols, x, y, k);
+    return 0;
+}
+
+/* One histogram over a window (an independent image with its own clamp). */
+static void hist_win(const uint8_t* px, int pitch, int x0, int y0, int rows, int cols, int k,
+                     const int* rank, uint64_t* hist) {
+    for (int x = x0; x < x0 + rows; ++x)
+        for (int y = y0; y < y0 + cols; ++y)
+            ++hist[rank[code_win(px, pitch, x0, y0, rows, cols, x, y, k)]];
+}
+
+static void rank_table(int k, int* rank) {
+    for (int c = 0; c < 256; ++c) rank[c] = oracle_bin_index(c, k);
+}
+
+/* descriptors.cpp:123-139 (k == 3 there; any k in [1,7] here, C(8,k) bins). */
+int oracle_histogram(const uint8_t* px, int rows, int cols, int k, uint64_t* hist) {
+    if (k < 1 || k > 7 || rows < 3 || cols < 3) return -1;
+    int rank[256];
+    rank_table(k, rank);
+    memset(hist, 0, sizeof(uint64_t) * (size_t)oracle_n_bins(k));
+    hist_win(px, cols, 0, 0, rows, cols, k, rank, hist);
+    return 0;
+}
+
+/* windowing.cpp:8-19,35-63 generalised to cell_rows x cell_cols cells:
+ * grid = floor(rows / cell_rows) x floor(cols / cell_cols), remainder
+ * dropped, cells row-major, each cell clamped as an independent image.
+ * hist is [grid_rows * grid_cols][n_bins]. Returns the number of cells, or
+ * -1 on invalid arguments (window < 3 or larger than the image throws in
+ * make_grid, windowing.cpp:9-17). */
+int oracle_cell_histograms(const uint8_t* px, int rows, int cols, int cell_rows,
+                           int cell_cols, int k, uint64_t* hist) {
+    if (k < 1 || k > 7 || rows < 3 || cols < 3) return -1;
+    if (cell_rows < 3 || cell_cols < 3 || cell_rows > rows || cell_cols > cols) return -1;
+    const int gr = rows / cell_rows, gc = cols / cell_cols, nb = oracle_n_bins(k);
+    int rank[256];
+    rank_table(k, rank);
+    memset(hist, 0, sizeof(uint64_t) * (size_t)gr * gc * nb);
+    for (int r = 0; r < gr; ++r)
+        for (int c = 0; c < gc; ++c)
+            hist_win(px, cols, r * cell_rows, c * cell_cols, cell_rows, cell_cols, k, rank,
+                     hist + ((size_t)r * gc + c) * nb);
+    return gr * gc;
+}
+
+/* ---- threaded batch driver (CPU baseline "port" leg and fast parity) ----
+ * Images are independent (SPEC: functions are pure), so a batch shards by
+ * image over `threads` POSIX threads. pixels: n x rows x cols contiguous;
+ * codes (nullable): same layout; hist (nullable): n x cells x n_bins (u64).
+ * cell_rows == 0 means one whole-image histogram per image. */
+typedef struct {
+    const uint8_t* px; int rows, cols, k, cell_rows, cell_cols;
+    uint8_t* codes; uint64_t* hist; int64_t first, last; int cells, nb;
+} batch_job;
+
+static void* batch_worker(void* arg) {
+    batch_job* j = (batch_job*)arg;
+    const size_t plane = (size_t)j->rows * (size_t)j->cols;
+    for (int64_t i = j->first; i < j->last; ++i) {
+        const uint8_t* img = j->px + (size_t)i * plane;
+        if (j->codes) oracle_code_map(img, j->rows, j->cols, j->k, j->codes + (size_t)i * plane);
+        if (j->hist) {
+            uint64_t* h = j->hist + (size_t)i * (size_t)j->cells * (size_t)j->nb;
+            if (j->cell_rows == 0) oracle_histogram(img, j->rows, j->cols, j->k, h);
+            else oracle_cell_histograms(img, j->rows, j->cols, j->cell_rows, j->cell_cols, j->k, h);
+        }
+    }
+    return NULL;
+}
+
+int oracle_batch(const uint8_t* px, int64_t n, int rows, int cols, int k, int cell_rows,
+                 int cell_cols, uint8_t* codes, uint64_t* hist, int threads) {
+    if (k < 1 || k > 7 || rows < 3 || cols < 3 || n < 0) return -1;
+    int cells = 1;
+    if (cell_rows != 0) {
+        if (cell_rows < 3 || cell_cols < 3 || cell_rows > rows || cell_cols > cols) return -1;
+        cells = (rows / cell_rows) * (cols / cell_cols);
+    }
+    if (threads < 1) threads = 1;
+    if (threads > 256) threads = 256;
+    if ((int64_t)threads > n) threads = (int)(n > 0 ? n : 1);
+    pthread_t tid[256];
+    batch_job jobs[256];
+    build_masks();
+    for (int t = 0; t < threads; ++t) {
+        jobs[t] = (batch_job){px, rows, cols, k, cell_rows, cell_cols, codes, hist,
+                              n * t / threads, n * (t + 1) / threads, cells, oracle_n_bins(k)};
+        pthread_create(&tid[t], NULL, batch_worker, &jobs[t]);
+    }
+    for (int t = 0; t < threads; ++t) pthread_join(tid[t], NULL);
+    return 0;
+}

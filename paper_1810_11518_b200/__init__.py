@@ -1,0 +1,306 @@
+"""B200-native LDP feature extraction (arxiv 1810.11518, ALDP) -- Python host layer.
+
+This package is the Python mirror of the reference's public LDP interface
+(reference tree ``proj/include/aldp``), sitting on the C-ABI of
+``libaldp_b200.so`` (declared in ``include/aldp_cuda.h``):
+
+================================  ===========================================
+this module                       reference
+================================  ===========================================
+``ldp_histogram(img, k, path)``   ``aldp::ldp_histogram`` (descriptors.hpp:55)
+``windowed_features(img, w, d)``  ``aldp::windowed_features`` (windowing.hpp:34)
+``ldp_code_map(img, k, path)``    new: the per-pixel code of descriptors.cpp:129-136
+``make_grid(img, window)``        ``aldp::make_grid`` (windowing.hpp:25)
+``n_bins(k)`` / ``ResponsePath``  bin layout (descriptors.cpp:25-45), kirsch.hpp:88
+``ldp_batch(...)``                device-resident batch (the hot path)
+================================  ===========================================
+
+Errors follow the reference: ``std::invalid_argument`` -> ``ValueError``,
+``std::out_of_range`` -> ``IndexError``, CUDA failures -> ``RuntimeError``.
+
+There is no CPU fallback: importing this package loads the CUDA library and
+raises if it is missing; every compute call runs the sm_100a kernels.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+import os
+from dataclasses import dataclass
+from typing import Optional, Tuple
+
+import numpy as np
+
+__all__ = [
+    "ResponsePath", "Descriptor", "AldpError", "lib", "LIB_PATH", "n_bins", "grid_cells",
+    "WindowGrid", "make_grid", "ldp_histogram", "windowed_features", "ldp_code_map",
+    "ldp_batch", "ldp_batch_host", "gen_faces", "gen_ties", "version",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libaldp_b200.so")
+
+
+class ResponsePath(enum.IntEnum):
+    """aldp::ResponsePath (kirsch.hpp:88). Both run the same B200 kernel:
+    their outputs are identical by contract (descriptors.hpp:53-54)."""
+    Naive = 0
+    Accelerated = 1
+
+
+class Descriptor(enum.Enum):
+    """aldp::Descriptor (descriptors.hpp:13). Lbp is not on the B200 path."""
+    Lbp = "LBP"
+    Ldp = "LDP"
+    Aldp = "ALDP"
+
+
+def parse_descriptor(name: str) -> Descriptor:
+    """aldp::parse_descriptor (descriptors.cpp:53-81), case-insensitive."""
+    for d in Descriptor:
+        if name.lower() == d.value.lower():
+            return d
+    raise ValueError(f"unknown descriptor '{name}' (expected lbp, ldp or aldp)")
+
+
+class AldpError(RuntimeError):
+    pass
+
+
+_STATUS_EXC = {1: ValueError, 2: IndexError, 3: AldpError, 4: MemoryError}
+
+
+class _Args(ctypes.Structure):
+    _fields_ = [
+        ("d_pixels", ctypes.c_void_p), ("img_stride", ctypes.c_int64),
+        ("rows", ctypes.c_int), ("cols", ctypes.c_int), ("pitch", ctypes.c_int),
+        ("n_images", ctypes.c_int), ("k", ctypes.c_int),
+        ("cell_rows", ctypes.c_int), ("cell_cols", ctypes.c_int),
+        ("d_codes", ctypes.c_void_p), ("codes_img_stride", ctypes.c_int64),
+        ("codes_pitch", ctypes.c_int), ("d_hist", ctypes.c_void_p),
+    ]
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    P, I, I64, U64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_uint64
+    sig = {
+        "aldp_ldp_batch": ([ctypes.POINTER(_Args), P], I),
+        "aldp_ldp_batch_ex": ([ctypes.POINTER(_Args), I, P], I),
+        "aldp_n_bins": ([I], I),
+        "aldp_grid_cells": ([I, I, I, I], I64),
+        "aldp_ldp_histogram": ([P, I, I, I, I, P], I),
+        "aldp_windowed_features": ([P, I, I, I, I, P, ctypes.c_size_t], I),
+        "aldp_ldp_code_map": ([P, I, I, I, I, P], I),
+        "aldp_ldp_batch_host": ([P, I, I, I, I, I, I, P, P, P], I),
+        "aldp_last_error": ([], ctypes.c_char_p),
+        "aldp_gen_faces": ([P, I, I, I, I, I64, I, U64, I64, P], I),
+        "aldp_gen_ties": ([P, I, I, I, I, I64, U64, I64, P], I),
+        "aldp_version": ([], ctypes.c_char_p),
+    }
+    for name, (argtypes, restype) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = argtypes
+        fn.restype = restype
+    return L
+
+
+lib = _load()
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        msg = lib.aldp_last_error().decode(errors="replace")
+        raise _STATUS_EXC.get(status, AldpError)(msg)
+
+
+def version() -> str:
+    return lib.aldp_version().decode()
+
+
+def n_bins(k: int) -> int:
+    """C(8, k) bins (56 for the reference's k == 3)."""
+    n = lib.aldp_n_bins(int(k))
+    if n == 0:
+        raise ValueError("k must be in [1, 7]")
+    return n
+
+
+def grid_cells(rows: int, cols: int, cell_rows: int, cell_cols: int) -> int:
+    n = lib.aldp_grid_cells(rows, cols, cell_rows, cell_cols)
+    if n < 0:
+        raise ValueError("invalid cell size for this image")
+    return int(n)
+
+
+@dataclass(frozen=True)
+class WindowGrid:
+    """aldp::WindowGrid (windowing.hpp:14-23)."""
+    window: int
+    grid_rows: int
+    grid_cols: int
+
+    def total(self) -> int:
+        return self.grid_rows * self.grid_cols
+
+
+def make_grid(img: np.ndarray, window: int) -> WindowGrid:
+    """aldp::make_grid (windowing.cpp:8-19): floor grid of square windows."""
+    rows, cols = img.shape
+    if window < 3:
+        raise ValueError(f"window side must be >= 3, got {window}")
+    if window > rows or window > cols:
+        raise ValueError(f"window side {window} exceeds image {rows}x{cols}")
+    return WindowGrid(window, rows // window, cols // window)
+
+
+def _as_image(img) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(img, dtype=np.uint8))
+    if a.ndim != 2:
+        raise ValueError("expected a 2-D uint8 image (rows x cols)")
+    return a
+
+
+def _path_value(path) -> int:
+    if isinstance(path, str):
+        path = ResponsePath.Naive if path.lower() in ("naive", "ldp") else ResponsePath.Accelerated
+    return int(path)
+
+
+def ldp_histogram(img, k: int = 3, path=ResponsePath.Accelerated) -> np.ndarray:
+    """aldp::ldp_histogram: 56 uint64 bins over every pixel (clamped borders)."""
+    a = _as_image(img)
+    out = np.zeros(56, dtype=np.uint64)
+    _check(lib.aldp_ldp_histogram(a.ctypes.data, a.shape[0], a.shape[1], int(k), _path_value(path),
+                                  out.ctypes.data))
+    return out
+
+
+def windowed_features(img, window: int, descriptor=Descriptor.Aldp) -> np.ndarray:
+    """aldp::windowed_features for Ldp/Aldp: [grid cells, 56] uint64, row-major
+    windows, each window clamped as an independent image."""
+    if isinstance(descriptor, str):
+        descriptor = parse_descriptor(descriptor)
+    if descriptor is Descriptor.Lbp:
+        raise NotImplementedError("LBP is not on the B200 LDP path (SURVEY.md 8f)")
+    a = _as_image(img)
+    grid = make_grid(a, window)
+    out = np.zeros((grid.total(), 56), dtype=np.uint64)
+    path = ResponsePath.Naive if descriptor is Descriptor.Ldp else ResponsePath.Accelerated
+    _check(lib.aldp_windowed_features(a.ctypes.data, a.shape[0], a.shape[1], int(window), int(path),
+                                      out.ctypes.data, out.size))
+    return out
+
+
+def ldp_code_map(img, k: int = 3, path=ResponsePath.Accelerated) -> np.ndarray:
+    """Code map (new entry point): codes[x, y] = ldp_code(responses(img, x, y), k)."""
+    a = _as_image(img)
+    out = np.zeros_like(a)
+    _check(lib.aldp_ldp_code_map(a.ctypes.data, a.shape[0], a.shape[1], int(k), _path_value(path),
+                                 out.ctypes.data))
+    return out
+
+
+def ldp_batch_host(pixels: np.ndarray, k: int = 3, cell: Tuple[int, int] = (0, 0),
+                   codes: bool = True, hist: bool = True, stream: int = 0):
+    """Host batch [n, rows, cols] uint8 -> (codes [n, rows, cols] | None,
+    hist uint32 [n, cells, n_bins] | None). H2D, kernel and D2H in one call."""
+    px = np.ascontiguousarray(pixels, dtype=np.uint8)
+    if px.ndim == 2:
+        px = px[None]
+    n, rows, cols = px.shape
+    nb = n_bins(k)
+    cells = grid_cells(rows, cols, *cell)
+    c = np.empty_like(px) if codes else None
+    h = np.empty((n, cells, nb), dtype=np.uint32) if hist else None
+    _check(lib.aldp_ldp_batch_host(px.ctypes.data, n, rows, cols, int(k), int(cell[0]), int(cell[1]),
+                                   c.ctypes.data if c is not None else None,
+                                   h.ctypes.data if h is not None else None, stream or None))
+    return c, h
+
+
+_KERNEL = {"auto": 0, "fast": 1, "generic": 2}
+
+
+def ldp_batch(pixels, rows: int, cols: int, k: int = 3, cell: Tuple[int, int] = (0, 0),
+              codes=None, hist=None, kernel: str = "auto", stream: Optional[int] = None):
+    """Device-resident batch (the hot path).
+
+    pixels: torch.uint8 CUDA tensor [n, rows, pitch] (contiguous; pitch >= cols).
+    codes:  None, True (allocate) or a torch.uint8 tensor [n, rows, codes_pitch].
+    hist:   None, True (allocate) or a torch.int32/uint32 tensor [n, cells, n_bins].
+    stream: a raw cudaStream_t (int); default: torch's current stream.
+    Returns (codes, hist). Asynchronous on the stream.
+    """
+    import torch
+    if pixels.dtype != torch.uint8 or not pixels.is_cuda or pixels.dim() != 3:
+        raise ValueError("pixels must be a CUDA uint8 tensor [n, rows, pitch]")
+    if not pixels.is_contiguous():
+        raise ValueError("pixels must be contiguous")
+    n, r, pitch = pixels.shape
+    if r != rows or pitch < cols:
+        raise ValueError("pixels shape does not match rows/cols")
+    nb = n_bins(k)
+    cells = grid_cells(rows, cols, *cell)
+    if codes is True:
+        codes = torch.empty((n, rows, pitch), dtype=torch.uint8, device=pixels.device)
+    if hist is True:
+        hist = torch.empty((n, cells, nb), dtype=torch.int32, device=pixels.device)
+    a = _Args()
+    a.d_pixels = pixels.data_ptr()
+    a.img_stride = rows * pitch
+    a.rows, a.cols, a.pitch, a.n_images, a.k = rows, cols, pitch, n, int(k)
+    a.cell_rows, a.cell_cols = int(cell[0]), int(cell[1])
+    if codes is not None:
+        if codes.dtype != torch.uint8 or codes.dim() != 3 or not codes.is_contiguous():
+            raise ValueError("codes must be a contiguous uint8 tensor [n, rows, pitch]")
+        a.d_codes = codes.data_ptr()
+        a.codes_pitch = codes.shape[2]
+        a.codes_img_stride = codes.shape[1] * codes.shape[2]
+    if hist is not None:
+        if hist.numel() < n * cells * nb or not hist.is_contiguous():
+            raise ValueError("hist tensor too small or not contiguous")
+        a.d_hist = hist.data_ptr()
+    if stream is None:
+        stream = torch.cuda.current_stream(pixels.device).cuda_stream
+    _check(lib.aldp_ldp_batch_ex(ctypes.byref(a), _KERNEL[kernel], stream or None))
+    return codes, hist
+
+
+def _pitch(cols: int, pitch: Optional[int]) -> int:
+    return pitch if pitch else (cols + 15) // 16 * 16
+
+
+def gen_faces(n: int, rows: int, cols: int, blobs: int = 20, seed: int = 1810,
+              first_index: int = 0, pitch: Optional[int] = None, device="cuda", out=None,
+              stream: Optional[int] = None):
+    """Face-like synthetic images on the device (BASELINE.json configs 2/4/5):
+    torch.uint8 [n, rows, pitch], keyed by (seed, first_index + i)."""
+    import torch
+    pitch = _pitch(cols, pitch)
+    if out is None:
+        out = torch.zeros((n, rows, pitch), dtype=torch.uint8, device=device)
+    if stream is None:
+        stream = torch.cuda.current_stream(out.device).cuda_stream
+    _check(lib.aldp_gen_faces(out.data_ptr(), n, rows, cols, pitch, rows * pitch, blobs, seed,
+                              first_index, stream or None))
+    return out
+
+
+def gen_ties(n: int, rows: int, cols: int, seed: int = 11518, first_index: int = 0,
+             pitch: Optional[int] = None, device="cuda", out=None, stream: Optional[int] = None):
+    """Tie-heavy synthetic images on the device (config 3): values {0,1,2}
+    with ~50% of the area under constant rectangles."""
+    import torch
+    pitch = _pitch(cols, pitch)
+    if out is None:
+        out = torch.zeros((n, rows, pitch), dtype=torch.uint8, device=device)
+    if stream is None:
+        stream = torch.cuda.current_stream(out.device).cuda_stream
+    _check(lib.aldp_gen_ties(out.data_ptr(), n, rows, cols, pitch, rows * pitch, seed, first_index,
+                             stream or None))
+    return out

@@ -1,0 +1,178 @@
+// ldp_common.cuh -- shared device helpers for the B200 LDP kernels.
+//
+// Semantics (reference paths relative to the reference tree):
+//   ring order, clockwise from top-left            proj/src/kirsch.cpp:11-12
+//   mask i = base ring {-3,-3,5,5,5,-3,-3,-3}
+//            rotated by i                          proj/src/kirsch.cpp:15,25
+//   code: top-k by (response desc, index asc)      proj/src/descriptors.cpp:83-102
+//   bins: ascending rank among popcount-k codes    proj/src/descriptors.cpp:25-45
+//
+// Kirsch redundancy identity (verified against the reference by the parity
+// tests): with r_j the eight ring pixels and S_i the sum of mask i's three
+// "+5" pixels, r[(2-i)&7] + r[(3-i)&7] + r[(4-i)&7], and T the ring sum,
+//     m_i = 5*S_i - 3*(T - S_i) = 8*S_i - 3*T.
+// T is common to all eight responses, so ordering m equals ordering S, ties
+// included, and the code depends on S alone (10-bit values, 0..765).
+//
+// Unique keys: K_i = 64*S_i + W[i] with W strictly decreasing, so a larger
+// key means a larger response, or an equal response and a lower index --
+// exactly the reference's selection order. K fits in 16 bits (<= 49023), so
+// two pixels share one 32-bit register as u16x2 lanes, and the whole
+// selection runs on the full-rate VIMNMX/VIMNMX3.U16x2 min/max instructions.
+//
+// The six-bit tags W are chosen so that the XOR of the tags of any k-subset
+// (k != 4) is distinct: XOR-ing the k selected keys' low six bits yields a
+// 6-bit id that names the code. A 64-entry table maps id -> code; the
+// histogram is counted per id and remapped to bins at flush time.
+#pragma once
+#include <cstdint>
+
+namespace aldp_b200 {
+
+__host__ __device__ constexpr uint32_t kTag(int i) {
+    // W[0..7] = 53, 48, 43, 37, 25, 19, 17, 16 (strictly decreasing;
+    // triple-XOR distinct; see tests/test_host.py::test_tag_set_properties)
+    return i == 0 ? 53u : i == 1 ? 48u : i == 2 ? 43u : i == 3 ? 37u
+         : i == 4 ? 25u : i == 5 ? 19u : i == 6 ? 17u : 16u;
+}
+constexpr uint32_t kTagAllXor = 53u ^ 48u ^ 43u ^ 37u ^ 25u ^ 19u ^ 17u ^ 16u;
+constexpr int kKeyShift = 6;
+
+__host__ __device__ inline int popcount8(unsigned c) {
+    int n = 0;
+    for (int b = 0; b < 8; ++b) n += (c >> b) & 1u;
+    return n;
+}
+
+__host__ __device__ inline int binom(int n, int r) {
+    if (r < 0 || r > n) return 0;
+    int v = 1;
+    for (int i = 1; i <= r; ++i) v = v * (n - r + i) / i;
+    return v;
+}
+
+// Rank of `code` among popcount(code)-bit codes in ascending numeric order:
+// ascending value is colex order of the bit sets, rank = sum_j C(p_j, j) over
+// the set bit positions p_1 < p_2 < ... (descriptors.cpp:25-45 enumerates
+// the same order by scanning c = 0..255).
+__host__ __device__ inline int colex_rank(unsigned code) {
+    int rank = 0, j = 0;
+    for (int p = 0; p < 8; ++p)
+        if ((code >> p) & 1u) rank += binom(p, ++j);
+    return rank;
+}
+
+__host__ __device__ inline uint32_t tag_xor(unsigned code) {
+    uint32_t x = 0;
+    for (int i = 0; i < 8; ++i)
+        if ((code >> i) & 1u) x ^= kTag(i);
+    return x;
+}
+
+// ---- packed u16x2 min/max (VIMNMX / VIMNMX3 on sm_100a) ----
+__device__ __forceinline__ uint32_t vmax(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("max.u16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ uint32_t vmin(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("min.u16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ uint32_t vmax3(uint32_t a, uint32_t b, uint32_t c) {
+    return vmax(vmax(a, b), c);  // ptxas fuses into VIMNMX3.U16x2
+}
+__device__ __forceinline__ uint32_t vmin3(uint32_t a, uint32_t b, uint32_t c) {
+    return vmin(vmin(a, b), c);
+}
+
+// XOR of the low-six-bit tags of the top-k keys of K[0..7] (u16x2 lanes,
+// keys unique per lane). Returns the per-lane id in bits 0-5 / 16-21 plus
+// garbage in the other bits (callers mask).
+//
+// Top-3 set: split into halves {K0..K3}, {K4..K7}; a partial 4-sorter gives
+// each half's three largest a1>=a2>=a3 (a1 = max(p,r), {a2,a3} = {x,y} with
+// p/q = max/min(K0,K1), r/s = max/min(K2,K3), x = min(p,r), y = max(q,s));
+// the top three of the union are then the half-cleaner maxima
+// {max(a1,b3), max(a2,b2), max(a3,b1)}. 18 min/max per two pixels.
+template <int K>
+__device__ __forceinline__ uint32_t topk_id(const uint32_t (&k)[8]) {
+    static_assert(K >= 1 && K <= 7 && K != 4, "k == 4 uses the generic kernel");
+    if constexpr (K == 1) {
+        return vmax3(vmax3(k[0], k[1], k[2]), vmax3(k[3], k[4], k[5]), vmax(k[6], k[7]));
+    } else if constexpr (K == 7) {  // complement of the single smallest key
+        return kTagAllXor * 0x10001u ^
+               vmin3(vmin3(k[0], k[1], k[2]), vmin3(k[3], k[4], k[5]), vmin(k[6], k[7]));
+    } else {
+        const uint32_t pA = vmax(k[0], k[1]), qA = vmin(k[0], k[1]);
+        const uint32_t rA = vmax(k[2], k[3]), sA = vmin(k[2], k[3]);
+        const uint32_t pB = vmax(k[4], k[5]), qB = vmin(k[4], k[5]);
+        const uint32_t rB = vmax(k[6], k[7]), sB = vmin(k[6], k[7]);
+        const uint32_t xA = vmin(pA, rA), yA = vmax(qA, sA);
+        const uint32_t xB = vmin(pB, rB), yB = vmax(qB, sB);
+        if constexpr (K == 3) {
+            const uint32_t a3 = vmin(xA, yA), b3 = vmin(xB, yB);
+            const uint32_t c1 = vmax3(pA, rA, b3);
+            const uint32_t c2 = vmax3(xA, yA, vmax(xB, yB));
+            const uint32_t c3 = vmax3(a3, pB, rB);
+            return c1 ^ c2 ^ c3;
+        } else if constexpr (K == 2) {  // {max(a1,b2), max(a2,b1)}
+            const uint32_t a2 = vmax(xA, yA), b2 = vmax(xB, yB);
+            return vmax3(pA, rA, b2) ^ vmax3(a2, pB, rB);
+        } else if constexpr (K == 6) {  // complement of the two smallest
+            const uint32_t s2A = vmin(xA, yA), s2B = vmin(xB, yB);
+            return kTagAllXor * 0x10001u ^ vmin3(qA, sA, s2B) ^ vmin3(s2A, qB, sB);
+        } else {  // K == 5: complement of the three smallest (dual network)
+            const uint32_t s3A = vmax(xA, yA), s3B = vmax(xB, yB);
+            const uint32_t e1 = vmin3(qA, sA, s3B);
+            const uint32_t e2 = vmin3(xA, yA, vmin(xB, yB));
+            const uint32_t e3 = vmin3(s3A, qB, sB);
+            return kTagAllXor * 0x10001u ^ e1 ^ e2 ^ e3;
+        }
+    }
+}
+
+// Scalar ring -> code for arbitrary k (1..7), the reference's rule stated as
+// "bit i set iff fewer than k keys beat K_i" (keys unique).
+__device__ __forceinline__ unsigned ring_code(const int (&r)[8], int k) {
+    uint32_t key[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int s = r[(2 - i) & 7] + r[(3 - i) & 7] + r[(4 - i) & 7];
+        key[i] = (uint32_t(s) << kKeyShift) | kTag(i);
+    }
+    unsigned code = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        int beaten = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) beaten += key[j] > key[i];
+        code |= unsigned(beaten < k) << i;
+    }
+    return code;
+}
+
+// Ring offsets (dx = row, dy = col), clockwise from the top-left
+// (kirsch.cpp:11-12).
+__device__ __forceinline__ int ring_dx(int j) { return j <= 2 ? -1 : (j == 3 || j == 7) ? 0 : 1; }
+__device__ __forceinline__ int ring_dy(int j) {
+    return (j == 0 || j == 6 || j == 7) ? -1 : (j == 1 || j == 5) ? 0 : 1;
+}
+
+// Code at (x, y) with every neighbour clamped into [x_lo, x_hi] x [y_lo, y_hi]
+// (image.cpp:36-40 applied to the image, or to a cell as windowing.cpp:42
+// does by cropping).
+__device__ __forceinline__ unsigned clamped_code(const uint8_t* img, int pitch, int x, int y,
+                                                 int x_lo, int x_hi, int y_lo, int y_hi, int k) {
+    int r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int xx = min(max(x + ring_dx(j), x_lo), x_hi);
+        const int yy = min(max(y + ring_dy(j), y_lo), y_hi);
+        r[j] = __ldg(img + size_t(xx) * size_t(pitch) + size_t(yy));
+    }
+    return ring_code(r, k);
+}
+
+}  // namespace aldp_b200

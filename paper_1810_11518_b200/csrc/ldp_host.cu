@@ -1,0 +1,355 @@
+// ldp_host.cu -- host-buffer C-ABI entry points (the reference's public
+// functions as C calls) and the synthetic input generators.
+//
+// The host entry points copy pixels to the device, run aldp_ldp_batch on a
+// per-thread stream with per-thread cached device buffers (no allocation on
+// the steady-state path), and copy results back:
+//   aldp_ldp_histogram      <- aldp::ldp_histogram      (descriptors.hpp:55)
+//   aldp_windowed_features  <- aldp::windowed_features  (windowing.hpp:34-36)
+//   aldp_ldp_code_map       <- new (descriptors.cpp:129-136 per-pixel code)
+//   aldp_ldp_batch_host     <- batch of the above (end-to-end bench path)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstdint>
+#include <cstring>
+#include <string>
+
+#include "aldp_cuda.h"
+
+namespace aldp_b200 {
+
+aldp_status set_error(aldp_status s, const std::string& msg);  // ldp_kernels.cu
+
+static aldp_status hfail(aldp_status s, const std::string& msg) { return set_error(s, msg); }
+
+#define HOST_CUDA_TRY(expr)                                                                 \
+    do {                                                                                    \
+        cudaError_t _e = (expr);                                                            \
+        if (_e != cudaSuccess)                                                              \
+            return hfail(_e == cudaErrorMemoryAllocation ? ALDP_ENOMEM : ALDP_ECUDA,        \
+                         std::string(#expr) + ": " + cudaGetErrorString(_e));               \
+    } while (0)
+
+// Per host thread: a stream and grow-only device buffers.
+struct HostCtx {
+    int device = -1;
+    cudaStream_t stream = nullptr;
+    uint8_t* d_px = nullptr;
+    size_t px_cap = 0;
+    uint8_t* d_codes = nullptr;
+    size_t codes_cap = 0;
+    uint32_t* d_hist = nullptr;
+    size_t hist_cap = 0;
+    uint32_t* h_hist = nullptr;  // pinned staging for u32 -> u64 widening
+    size_t h_hist_cap = 0;
+    ~HostCtx() {
+        // Process teardown: the CUDA context may already be gone; ignore errors.
+        if (d_px) cudaFree(d_px);
+        if (d_codes) cudaFree(d_codes);
+        if (d_hist) cudaFree(d_hist);
+        if (h_hist) cudaFreeHost(h_hist);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+static thread_local HostCtx t_ctx;
+
+static aldp_status ensure(void** p, size_t* cap, size_t need) {
+    if (*cap >= need) return ALDP_OK;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    *cap = 0;
+    HOST_CUDA_TRY(cudaMalloc(p, need));
+    *cap = need;
+    return ALDP_OK;
+}
+
+static aldp_status ctx_ready(HostCtx& c) {
+    int dev = 0;
+    HOST_CUDA_TRY(cudaGetDevice(&dev));
+    if (c.device != dev) {
+        // a different device on this thread: drop buffers of the old one
+        if (c.d_px) cudaFree(c.d_px);
+        if (c.d_codes) cudaFree(c.d_codes);
+        if (c.d_hist) cudaFree(c.d_hist);
+        c.d_px = nullptr;
+        c.d_codes = nullptr;
+        c.d_hist = nullptr;
+        c.px_cap = c.codes_cap = c.hist_cap = 0;
+        if (c.stream) cudaStreamDestroy(c.stream);
+        c.stream = nullptr;
+        HOST_CUDA_TRY(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+        c.device = dev;
+    }
+    return ALDP_OK;
+}
+
+static int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+// Shared body: host pixels (n contiguous rows x cols images) -> optional host
+// codes (contiguous) and device-side u32 histograms copied to `hist32`.
+static aldp_status host_batch(const uint8_t* px, int n, int rows, int cols, int k, int cell_rows,
+                              int cell_cols, uint8_t* codes, uint32_t* hist32, cudaStream_t user) {
+    if (!px && n > 0) return hfail(ALDP_EINVAL, "null pixels");
+    if (n < 0) return hfail(ALDP_EINVAL, "negative image count");
+    if (rows < 3 || cols < 3)
+        return hfail(ALDP_EINVAL, "descriptor extraction needs at least a 3x3 image, got " +
+                                      std::to_string(rows) + "x" + std::to_string(cols));
+    const int nbins = aldp_n_bins(k);
+    if (nbins == 0) return hfail(ALDP_EINVAL, "k must be in [1, 7]");
+    const int64_t cells = aldp_grid_cells(rows, cols, cell_rows, cell_cols);
+    if (cells < 0) return hfail(ALDP_EINVAL, "invalid window/cell size for this image");
+    HostCtx& c = t_ctx;
+    aldp_status s = ctx_ready(c);
+    if (s != ALDP_OK) return s;
+    cudaStream_t st = user ? user : c.stream;
+    // pad the device pitch to 16 B so the packed kernel always applies
+    const int pitch = round_up(cols, 16);
+    const size_t img_bytes = size_t(pitch) * rows;
+    s = ensure(reinterpret_cast<void**>(&c.d_px), &c.px_cap, img_bytes * std::max(n, 1));
+    if (s != ALDP_OK) return s;
+    if (codes) {
+        s = ensure(reinterpret_cast<void**>(&c.d_codes), &c.codes_cap, img_bytes * std::max(n, 1));
+        if (s != ALDP_OK) return s;
+    }
+    const size_t hist_n = size_t(n) * cells * nbins;
+    if (hist32) {
+        s = ensure(reinterpret_cast<void**>(&c.d_hist), &c.hist_cap,
+                   sizeof(uint32_t) * std::max<size_t>(hist_n, 1));
+        if (s != ALDP_OK) return s;
+    }
+    if (n == 0) return ALDP_OK;
+    if (pitch == cols)
+        HOST_CUDA_TRY(cudaMemcpyAsync(c.d_px, px, img_bytes * n, cudaMemcpyHostToDevice, st));
+    else
+        HOST_CUDA_TRY(cudaMemcpy2DAsync(c.d_px, pitch, px, cols, cols, size_t(rows) * n,
+                                        cudaMemcpyHostToDevice, st));
+    aldp_ldp_args a{};
+    a.d_pixels = c.d_px;
+    a.img_stride = int64_t(img_bytes);
+    a.rows = rows;
+    a.cols = cols;
+    a.pitch = pitch;
+    a.n_images = n;
+    a.k = k;
+    a.cell_rows = cell_rows;
+    a.cell_cols = cell_cols;
+    a.d_codes = codes ? c.d_codes : nullptr;
+    a.codes_img_stride = int64_t(img_bytes);
+    a.codes_pitch = pitch;
+    a.d_hist = hist32 ? c.d_hist : nullptr;
+    s = aldp_ldp_batch(&a, st);
+    if (s != ALDP_OK) return hfail(s, aldp_last_error());
+    if (codes) {
+        if (pitch == cols)
+            HOST_CUDA_TRY(cudaMemcpyAsync(codes, c.d_codes, img_bytes * n, cudaMemcpyDeviceToHost, st));
+        else
+            HOST_CUDA_TRY(cudaMemcpy2DAsync(codes, cols, c.d_codes, pitch, cols, size_t(rows) * n,
+                                            cudaMemcpyDeviceToHost, st));
+    }
+    if (hist32)
+        HOST_CUDA_TRY(cudaMemcpyAsync(hist32, c.d_hist, sizeof(uint32_t) * hist_n,
+                                      cudaMemcpyDeviceToHost, st));
+    HOST_CUDA_TRY(cudaStreamSynchronize(st));
+    return ALDP_OK;
+}
+
+static aldp_status widen(const uint32_t* h32, uint64_t* h64, size_t n) {
+    for (size_t i = 0; i < n; ++i) h64[i] = h32[i];
+    return ALDP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// generators
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint64_t hash3(uint64_t seed, uint64_t a, uint64_t b) {
+    return mix64(mix64(mix64(seed) ^ a) ^ b);
+}
+__device__ __forceinline__ float u01(uint64_t h) {  // [0, 1)
+    return float(h >> 40) * (1.0f / 16777216.0f);
+}
+
+constexpr int kMaxBlobs = 256;
+constexpr int kMaxRects = 512;
+
+// grid: (row chunks, images); each CTA rebuilds its image's parameters.
+__global__ void gen_faces_kernel(uint8_t* out, int rows, int cols, int pitch, int64_t stride,
+                                 int blobs, uint64_t seed, int64_t first) {
+    __shared__ float bx[kMaxBlobs], by[kMaxBlobs], binv[kMaxBlobs], bamp[kMaxBlobs];
+    __shared__ float g[4];
+    const int64_t gidx = first + blockIdx.y;
+    const uint64_t is = hash3(seed, 0xFACEull, uint64_t(gidx));
+    for (int b = threadIdx.x; b < blobs; b += blockDim.x) {
+        bx[b] = u01(hash3(is, b, 1)) * rows;
+        by[b] = u01(hash3(is, b, 2)) * cols;
+        const float sigma = 5.0f + 55.0f * u01(hash3(is, b, 3));
+        binv[b] = -0.5f / (sigma * sigma);
+        bamp[b] = -80.0f + 160.0f * u01(hash3(is, b, 4));
+    }
+    if (threadIdx.x == 0) {
+        const float th = 6.2831853f * u01(hash3(is, 0x9A, 1));
+        const float lo = 40.0f + 80.0f * u01(hash3(is, 0x9A, 2));
+        const float hi = 120.0f + 100.0f * u01(hash3(is, 0x9A, 3));
+        // intensity = lo + (hi - lo) * t, t = projection on (cos, sin) in [0, 1]
+        const float cx = cosf(th), cy = sinf(th);
+        const float span = fabsf(cx) * (rows - 1) + fabsf(cy) * (cols - 1) + 1e-6f;
+        g[0] = cx * (hi - lo) / span;
+        g[1] = cy * (hi - lo) / span;
+        g[2] = lo - fminf(0.0f, cx * (rows - 1)) * (hi - lo) / span -
+               fminf(0.0f, cy * (cols - 1)) * (hi - lo) / span;
+        g[3] = 0.0f;
+    }
+    __syncthreads();
+    uint8_t* img = out + blockIdx.y * stride;
+    const int rows_per = (rows + gridDim.x - 1) / gridDim.x;
+    const int x0 = blockIdx.x * rows_per, x1 = min(rows, x0 + rows_per);
+    for (int64_t t = threadIdx.x; t < int64_t(x1 - x0) * cols; t += blockDim.x) {
+        const int x = x0 + int(t / cols), y = int(t % cols);
+        float v = g[2] + g[0] * x + g[1] * y;
+        for (int b = 0; b < blobs; ++b) {
+            const float dx = x - bx[b], dy = y - by[b];
+            v += bamp[b] * __expf((dx * dx + dy * dy) * binv[b]);
+        }
+        const uint64_t h = hash3(is, 0x7E57ull, uint64_t(x) * uint64_t(cols) + uint64_t(y));
+        const float u1 = fmaxf(u01(h), 1e-7f), u2 = float(uint32_t(h) >> 8) * (1.0f / 16777216.0f);
+        v += 6.0f * sqrtf(-2.0f * __logf(u1)) * __cosf(6.2831853f * u2);
+        img[int64_t(x) * pitch + y] = uint8_t(fminf(fmaxf(rintf(v), 0.0f), 255.0f));
+    }
+}
+
+__global__ void gen_ties_kernel(uint8_t* out, int rows, int cols, int pitch, int64_t stride,
+                                uint64_t seed, int64_t first) {
+    __shared__ int rx0[kMaxRects], ry0[kMaxRects], rx1[kMaxRects], ry1[kMaxRects];
+    __shared__ uint8_t rv[kMaxRects];
+    __shared__ int n_rects;
+    const int64_t gidx = first + blockIdx.y;
+    const uint64_t is = hash3(seed, 0x71E5ull, uint64_t(gidx));
+    if (threadIdx.x == 0) {
+        // paint until the summed rectangle area reaches ln 2 of the image, so
+        // the expected union of uniformly placed rectangles is ~50%
+        const double target = 0.6931 * double(rows) * cols;
+        double area = 0;
+        int n = 0;
+        const int side_max = max(4, min(rows, cols) / 4);
+        while (area < target && n < kMaxRects) {
+            const int h = 2 + int(u01(hash3(is, n, 1)) * side_max);
+            const int w = 2 + int(u01(hash3(is, n, 2)) * side_max);
+            const int x = int(u01(hash3(is, n, 3)) * rows), y = int(u01(hash3(is, n, 4)) * cols);
+            rx0[n] = x;
+            ry0[n] = y;
+            rx1[n] = min(rows, x + h);
+            ry1[n] = min(cols, y + w);
+            rv[n] = uint8_t(hash3(is, n, 5) % 3);
+            area += double(rx1[n] - x) * (ry1[n] - y);
+            ++n;
+        }
+        n_rects = n;
+    }
+    __syncthreads();
+    uint8_t* img = out + blockIdx.y * stride;
+    const int rows_per = (rows + gridDim.x - 1) / gridDim.x;
+    const int x0 = blockIdx.x * rows_per, x1 = min(rows, x0 + rows_per);
+    for (int64_t t = threadIdx.x; t < int64_t(x1 - x0) * cols; t += blockDim.x) {
+        const int x = x0 + int(t / cols), y = int(t % cols);
+        uint8_t v = uint8_t(hash3(is, 0xB1ull, uint64_t(x) * uint64_t(cols) + uint64_t(y)) % 3);
+        for (int r = n_rects - 1; r >= 0; --r)  // painter's order: last rectangle wins
+            if (x >= rx0[r] && x < rx1[r] && y >= ry0[r] && y < ry1[r]) {
+                v = rv[r];
+                break;
+            }
+        img[int64_t(x) * pitch + y] = v;
+    }
+}
+
+}  // namespace aldp_b200
+
+using namespace aldp_b200;
+
+extern "C" {
+
+aldp_status aldp_ldp_histogram(const uint8_t* pixels, int rows, int cols, int k, int path,
+                               uint64_t* bins56) {
+    (void)path;  // Naive and Accelerated are identical by contract (descriptors.hpp:53-54)
+    if (k != 3) return hfail(ALDP_EINVAL, "the 56-bin histogram layout requires k == 3");
+    uint32_t h32[56];
+    aldp_status s = host_batch(pixels, 1, rows, cols, 3, 0, 0, nullptr, h32, nullptr);
+    if (s != ALDP_OK) return s;
+    return widen(h32, bins56, 56);
+}
+
+aldp_status aldp_windowed_features(const uint8_t* pixels, int rows, int cols, int window,
+                                   int path, uint64_t* out, size_t out_len) {
+    (void)path;
+    if (window < 3) return hfail(ALDP_EINVAL, "window side must be >= 3, got " + std::to_string(window));
+    if (window > rows || window > cols)
+        return hfail(ALDP_EINVAL, "window side " + std::to_string(window) + " exceeds image " +
+                                      std::to_string(rows) + "x" + std::to_string(cols));
+    const int64_t cells = aldp_grid_cells(rows, cols, window, window);
+    if (out_len < size_t(cells) * 56) return hfail(ALDP_ERANGE, "output buffer too small");
+    uint32_t* h32 = static_cast<uint32_t*>(std::malloc(sizeof(uint32_t) * size_t(cells) * 56));
+    if (!h32) return hfail(ALDP_ENOMEM, "host allocation failed");
+    aldp_status s = host_batch(pixels, 1, rows, cols, 3, window, window, nullptr, h32, nullptr);
+    if (s == ALDP_OK) widen(h32, out, size_t(cells) * 56);
+    std::free(h32);
+    return s;
+}
+
+aldp_status aldp_ldp_code_map(const uint8_t* pixels, int rows, int cols, int k, int path,
+                              uint8_t* codes) {
+    (void)path;
+    if (!codes) return hfail(ALDP_EINVAL, "null codes buffer");
+    return host_batch(pixels, 1, rows, cols, k, 0, 0, codes, nullptr, nullptr);
+}
+
+aldp_status aldp_ldp_batch_host(const uint8_t* pixels, int n_images, int rows, int cols, int k,
+                                int cell_rows, int cell_cols, uint8_t* codes, uint32_t* hist,
+                                void* stream) {
+    return host_batch(pixels, n_images, rows, cols, k, cell_rows, cell_cols, codes, hist,
+                      static_cast<cudaStream_t>(stream));
+}
+
+aldp_status aldp_gen_faces(uint8_t* d_out, int n_images, int rows, int cols, int pitch,
+                           int64_t img_stride, int blobs, uint64_t seed, int64_t first_index,
+                           void* stream) {
+    if (n_images < 0 || rows < 1 || cols < 1 || pitch < cols || blobs < 0 || blobs > kMaxBlobs)
+        return hfail(ALDP_EINVAL, "gen_faces: bad arguments");
+    if (n_images == 0) return ALDP_OK;
+    const int chunks = std::max(1, std::min(rows, (rows * cols + 65535) / 65536));
+    // grid.y is limited to 65535: launch in slabs of images
+    for (int done = 0; done < n_images; done += 65535) {
+        const int cnt = std::min(65535, n_images - done);
+        gen_faces_kernel<<<dim3(chunks, cnt), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+            d_out + int64_t(done) * img_stride, rows, cols, pitch, img_stride, blobs, seed,
+            first_index + done);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return hfail(ALDP_ECUDA, std::string("gen_faces: ") + cudaGetErrorString(e));
+    return ALDP_OK;
+}
+
+aldp_status aldp_gen_ties(uint8_t* d_out, int n_images, int rows, int cols, int pitch,
+                          int64_t img_stride, uint64_t seed, int64_t first_index, void* stream) {
+    if (n_images < 0 || rows < 1 || cols < 1 || pitch < cols)
+        return hfail(ALDP_EINVAL, "gen_ties: bad arguments");
+    if (n_images == 0) return ALDP_OK;
+    const int chunks = std::max(1, std::min(rows, (rows * cols + 65535) / 65536));
+    for (int done = 0; done < n_images; done += 65535) {
+        const int cnt = std::min(65535, n_images - done);
+        gen_ties_kernel<<<dim3(chunks, cnt), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+            d_out + int64_t(done) * img_stride, rows, cols, pitch, img_stride, seed,
+            first_index + done);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return hfail(ALDP_ECUDA, std::string("gen_ties: ") + cudaGetErrorString(e));
+    return ALDP_OK;
+}
+
+}  // extern "C"

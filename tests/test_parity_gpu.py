@@ -1,0 +1,265 @@
+"""GPU parity: the B200 kernels, called through the C-ABI, against the CPU
+oracle (pinned in test_oracle.py) and the reference's golden vectors.
+Bit-exact for every code map and histogram."""
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_1810_11518_b200 as aldp  # noqa: E402
+
+DEV = torch.device("cuda:0")
+KERNELS = ("fast", "generic")
+
+
+def to_dev(px, pitch=None):
+    """[n, rows, cols] host -> [n, rows, pitch] device (pitch padded)."""
+    px = np.ascontiguousarray(px, np.uint8)
+    if px.ndim == 2:
+        px = px[None]
+    n, r, c = px.shape
+    pitch = pitch or (c + 15) // 16 * 16
+    buf = np.zeros((n, r, pitch), np.uint8)
+    buf[:, :, :c] = px
+    return torch.from_numpy(buf).to(DEV)
+
+
+def run(px_host, k=3, cell=(0, 0), kernel="auto", pitch=None):
+    px_host = np.ascontiguousarray(px_host, np.uint8)
+    if px_host.ndim == 2:
+        px_host = px_host[None]
+    n, r, c = px_host.shape
+    d = to_dev(px_host, pitch)
+    codes, hist = aldp.ldp_batch(d, r, c, k=k, cell=cell, codes=True, hist=True, kernel=kernel)
+    torch.cuda.synchronize()
+    return codes[:, :, :c].cpu().numpy(), hist.cpu().numpy().astype(np.uint64)
+
+
+# ------------------------------------------------------------- goldens
+
+def test_reference_golden_fixtures(golden_fixtures):
+    for fx in golden_fixtures:
+        img = np.array(fx["pixels"], np.uint8).reshape(fx["rows"], fx["cols"])
+        for kern in ("auto", "generic"):
+            codes, hist = run(img, 3, kernel=kern)
+            assert list(codes.ravel()) == fx["ldp_codes"], (fx["name"], kern)
+            assert list(hist[0, 0]) == fx["ldp_histogram"], (fx["name"], kern)
+
+
+def test_reference_library_vectors_all_k(ref_vectors):
+    names = sorted({k.rsplit("_", 1)[0] for k in ref_vectors if k.endswith("_img") and
+                    not k.startswith("win")})
+    for nm in names:
+        img = ref_vectors[nm + "_img"]
+        for k in range(1, 8):
+            codes, hist = run(img, k)
+            assert np.array_equal(codes[0], ref_vectors[nm + "_codes"][k - 1]), (nm, k)
+            if k == 3:
+                assert np.array_equal(hist[0, 0], ref_vectors[nm + "_hist"]), nm
+
+
+def test_reference_windowed_vectors(ref_vectors):
+    img = ref_vectors["win_img"]
+    for w in (3, 10, 25, 32, 64, 96):
+        for kern in ("auto", "generic"):
+            _, hist = run(img, 3, cell=(w, w), kernel=kern)
+            assert np.array_equal(hist[0], ref_vectors[f"win{w}"]), (w, kern)
+
+
+def test_config1_digest(ref_vectors):
+    """C1: make_random(490, 640, 42), k=3, code map + whole-image histogram."""
+    import hashlib
+    img = oracle.make_random(490, 640, 42)
+    for kern in KERNELS:
+        codes, hist = run(img, 3, kernel=kern)
+        assert hashlib.sha256(codes[0].tobytes()).digest() == ref_vectors["c1_codes_sha256"].tobytes()
+        assert np.array_equal(hist[0, 0], ref_vectors["c1_hist"])
+
+# ------------------------------------------------ seeded parity vs oracle
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 6, 7])
+def test_random_images_every_k(k):
+    rng = np.random.default_rng(100 + k)
+    for shape in [(3, 4), (3, 3), (5, 8), (17, 64), (33, 132), (64, 256), (7, 13), (31, 29)]:
+        img = rng.integers(0, 256, size=shape, dtype=np.uint8)
+        want_c, want_h = oracle.batch(img, k=k)
+        for kern in ("auto", "generic"):
+            c, h = run(img, k, kernel=kern)
+            assert np.array_equal(c, want_c), (shape, k, kern)
+            assert np.array_equal(h, want_h), (shape, k, kern)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 5, 6, 7])
+def test_tie_heavy_every_k(k):
+    """Values {0,1,2} with constant rectangles (config-3 style)."""
+    px = aldp.gen_ties(6, 64, 128, seed=7 + k, device=DEV)
+    torch.cuda.synchronize()
+    host = px[:, :, :128].cpu().numpy()
+    want_c, want_h = oracle.batch(host, k=k)
+    for kern in KERNELS:
+        c, h = run(host, k, kernel=kern)
+        assert np.array_equal(c, want_c), (k, kern)
+        assert np.array_equal(h, want_h), (k, kern)
+
+
+@pytest.mark.parametrize("cell", [(3, 3), (8, 12), (16, 16), (64, 64), (81, 91), (40, 128), (33, 70),
+                                  (100, 100)])
+def test_cell_histograms(cell):
+    """windowed_features semantics: each cell clamped as its own image."""
+    rng = np.random.default_rng(cell[0] * 1000 + cell[1])
+    img = rng.integers(0, 256, size=(3, 200, 256), dtype=np.uint8)
+    want_c, want_h = oracle.batch(img, k=3, cell=cell)
+    for kern in ("auto", "generic"):
+        c, h = run(img, 3, cell=cell, kernel=kern)
+        assert np.array_equal(c, want_c), (cell, kern)
+        assert np.array_equal(h, want_h), (cell, kern)
+
+
+def test_cell_histograms_k_sweep():
+    px = aldp.gen_faces(2, 162, 182, blobs=8, seed=3, device=DEV)
+    torch.cuda.synchronize()
+    host = px[:, :, :182].cpu().numpy()
+    for k in (1, 2, 3, 5, 6, 7):
+        want_c, want_h = oracle.batch(host, k=k, cell=(81, 91))
+        c, h = run(host, k, cell=(81, 91), kernel="fast")
+        assert np.array_equal(c, want_c), k
+        assert np.array_equal(h, want_h), k
+
+
+def test_odd_pitch_and_strides():
+    rng = np.random.default_rng(9)
+    img = rng.integers(0, 256, size=(4, 50, 96), dtype=np.uint8)
+    want_c, want_h = oracle.batch(img, k=3, cell=(10, 12))
+    c, h = run(img, 3, cell=(10, 12), pitch=100)  # pitch % 16 != 0, % 4 == 0 -> fast
+    assert np.array_equal(c, want_c) and np.array_equal(h, want_h)
+    c, h = run(img, 3, cell=(10, 12), pitch=97)   # unaligned pitch -> generic
+    assert np.array_equal(c, want_c) and np.array_equal(h, want_h)
+
+
+def test_config2_subset():
+    """C2 generator (face-like 640x490), 7x6 cells, 64 images."""
+    px = aldp.gen_faces(64, 490, 640, blobs=20, seed=1810, device=DEV)
+    codes, hist = aldp.ldp_batch(px, 490, 640, k=3, cell=(81, 91), codes=True, hist=True)
+    torch.cuda.synchronize()
+    host = px.cpu().numpy()
+    want_c, want_h = oracle.batch(host, k=3, cell=(81, 91))
+    assert np.array_equal(codes.cpu().numpy(), want_c)
+    assert np.array_equal(hist.cpu().numpy().astype(np.uint64), want_h)
+    assert int(hist.sum()) == 64 * 42 * 81 * 91
+
+
+def test_config3_subset_k_sweep():
+    px = aldp.gen_ties(4, 1024, 1024, seed=11518, device=DEV)
+    torch.cuda.synchronize()
+    host = px.cpu().numpy()
+    for k in (1, 3, 5):
+        want_c, want_h = oracle.batch(host, k=k)
+        codes, hist = aldp.ldp_batch(px, 1024, 1024, k=k, codes=True, hist=True)
+        torch.cuda.synchronize()
+        assert np.array_equal(codes.cpu().numpy(), want_c), k
+        assert np.array_equal(hist.cpu().numpy().astype(np.uint64), want_h), k
+
+
+def test_config4_full_size_sampled():
+    """C4 (16384^2, 64x64 cells) at full size: size-independent properties on
+    the whole frame + bit-exact oracle checks on sampled cells and bands."""
+    n = 16384
+    px = aldp.gen_faces(1, n, n, blobs=200, seed=42, device=DEV)
+    codes, hist = aldp.ldp_batch(px, n, n, k=3, cell=(64, 64), codes=True, hist=True)
+    _, whole = aldp.ldp_batch(px, n, n, k=3, hist=True)
+    torch.cuda.synchronize()
+    h = hist[0].to(torch.int64)
+    assert int(h.sum()) == n * n
+    assert bool((h.sum(dim=1) == 64 * 64).all())
+    # whole-image histogram == histogram of the code map (descriptors.cpp:129-137)
+    cm = torch.bincount(codes[0].reshape(-1).to(torch.int64), minlength=256)
+    rank = [c for c in range(256) if bin(c).count("1") == 3]
+    assert torch.equal(cm[rank].cpu(), whole[0, 0].to(torch.int64).cpu())
+    assert int(cm.sum()) == n * n and int(cm[[c for c in range(256) if bin(c).count("1") != 3]].sum()) == 0
+    rng = np.random.default_rng(4)
+    for _ in range(24):  # cells: each is an independent image (per-cell clamp)
+        i, j = rng.integers(0, 256, size=2)
+        crop = px[0, i * 64:(i + 1) * 64, j * 64:(j + 1) * 64].cpu().numpy()
+        assert np.array_equal(h[i * 256 + j].cpu().numpy().astype(np.uint64), oracle.histogram(crop, 3))
+    for x0 in (0, 4095, 8190, n - 40):  # row bands of the code map (image clamp)
+        a, b = max(x0 - 1, 0), min(x0 + 41, n)
+        band = px[0, a:b].cpu().numpy()
+        want = oracle.code_map(band, 3)
+        got = codes[0, a:b].cpu().numpy()
+        inner = slice(1 if a > 0 else 0, (b - a) - (1 if b < n else 0))
+        assert np.array_equal(got[inner], want[inner]), x0
+
+
+def test_fast_equals_generic_on_faces():
+    px = aldp.gen_faces(8, 200, 320, blobs=12, seed=5, device=DEV)
+    for cell in ((0, 0), (50, 64), (81, 91)):
+        c1, h1 = aldp.ldp_batch(px, 200, 320, cell=cell, codes=True, hist=True, kernel="fast")
+        c2, h2 = aldp.ldp_batch(px, 200, 320, cell=cell, codes=True, hist=True, kernel="generic")
+        torch.cuda.synchronize()
+        assert torch.equal(c1, c2) and torch.equal(h1, h2), cell
+
+
+def test_generator_determinism_and_sharding():
+    """Images are keyed by global index: any shard split sees identical bytes."""
+    a = aldp.gen_faces(6, 49, 64, blobs=5, seed=99, first_index=0, device=DEV)
+    b = aldp.gen_faces(3, 49, 64, blobs=5, seed=99, first_index=3, device=DEV)
+    c = aldp.gen_faces(6, 49, 64, blobs=5, seed=99, first_index=0, device=DEV)
+    torch.cuda.synchronize()
+    assert torch.equal(a, c) and torch.equal(a[3:], b)
+    t1 = aldp.gen_ties(4, 64, 64, seed=1, device=DEV)
+    t2 = aldp.gen_ties(2, 64, 64, seed=1, first_index=2, device=DEV)
+    torch.cuda.synchronize()
+    assert torch.equal(t1[2:], t2)
+    assert int(t1.max()) <= 2
+
+
+# ------------------------------------------------ host entry points (C-ABI)
+
+def test_host_entry_points_match_oracle():
+    img = oracle.make_random(37, 53, 5)
+    assert np.array_equal(aldp.ldp_histogram(img, 3, aldp.ResponsePath.Naive),
+                          oracle.ref_ldp_histogram(img, 3, 0))
+    assert np.array_equal(aldp.ldp_histogram(img, 3), oracle.ref_ldp_histogram(img, 3, 1))
+    for w in (3, 8, 37):
+        assert np.array_equal(aldp.windowed_features(img, w, "ldp"), oracle.ref_windowed(img, w, 0))
+        assert np.array_equal(aldp.windowed_features(img, w, aldp.Descriptor.Aldp), oracle.ref_windowed(img, w, 1))
+    for k in range(1, 8):
+        assert np.array_equal(aldp.ldp_code_map(img, k), oracle.code_map(img, k))
+    c, h = aldp.ldp_batch_host(np.stack([img, img[::-1].copy()]), k=3, cell=(9, 10))
+    wc, wh = oracle.batch(np.stack([img, img[::-1].copy()]), k=3, cell=(9, 10))
+    assert np.array_equal(c, wc) and np.array_equal(h.astype(np.uint64), wh)
+
+
+def test_host_entry_point_errors():
+    img = np.zeros((10, 10), np.uint8)
+    with pytest.raises(ValueError):
+        aldp.ldp_histogram(img, 2)                    # k != 3 (descriptors.cpp:124-126)
+    with pytest.raises(ValueError):
+        aldp.ldp_histogram(np.zeros((2, 9), np.uint8), 3)  # < 3x3
+    with pytest.raises(ValueError):
+        aldp.windowed_features(img, 2)                # window < 3
+    with pytest.raises(ValueError):
+        aldp.windowed_features(img, 11)               # window > image
+    with pytest.raises(ValueError):
+        aldp.ldp_code_map(img, 8)                     # k out of [1, 7]
+    px = to_dev(img)
+    with pytest.raises(ValueError):
+        aldp.ldp_batch(px, 10, 10, k=4, cell=(5, 5), codes=True, hist=True, kernel="fast")
+
+
+def test_empty_batch_and_constant_images():
+    px = torch.zeros((0, 8, 16), dtype=torch.uint8, device=DEV)
+    c, h = aldp.ldp_batch(px, 8, 16, codes=True, hist=True)
+    torch.cuda.synchronize()
+    assert c.numel() == 0 and h.numel() == 0
+    const = torch.full((2, 10, 16), 200, dtype=torch.uint8, device=DEV)
+    c, h = aldp.ldp_batch(const, 10, 16, codes=True, hist=True)
+    torch.cuda.synchronize()
+    assert bool((c[:, :, :16] == 7).all())            # total tie -> code 7 (bin 0)
+    assert int(h[0, 0, 0]) == 160 and int(h.sum()) == 320
