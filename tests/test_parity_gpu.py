@@ -122,9 +122,9 @@ def test_cell_histograms(cell):
 
 
 def test_cell_histograms_k_sweep():
-    px = aldp.gen_faces(2, 162, 182, blobs=8, seed=3, device=DEV)
+    px = aldp.gen_faces(2, 162, 184, blobs=8, seed=3, device=DEV)
     torch.cuda.synchronize()
-    host = px[:, :, :182].cpu().numpy()
+    host = px[:, :, :184].cpu().numpy()
     for k in (1, 2, 3, 5, 6, 7):
         want_c, want_h = oracle.batch(host, k=k, cell=(81, 91))
         c, h = run(host, k, cell=(81, 91), kernel="fast")
