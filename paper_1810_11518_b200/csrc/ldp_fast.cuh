@@ -43,6 +43,7 @@ constexpr int kRegion = 512;
 constexpr int kSegRegions = kMaxTileCells + 1;
 constexpr int kWarpSmem = 2 * kSegRegions * kRegion;  // 4 KB
 constexpr int kFixList = 16;                           // fix columns per segment (max)
+constexpr int kL2Ahead = 12;                           // rows of L2 prefetch ahead of the load
 
 struct FastParams {
     const uint8_t* px;
@@ -128,7 +129,7 @@ __device__ __forceinline__ void red_shared(uint32_t addr) {
 }
 
 template <int K, bool CELLS>
-__global__ void __launch_bounds__(kFastWarps * 32) ldp_fast_kernel(FastParams p) {
+__global__ void __launch_bounds__(kFastWarps * 32, 2) ldp_fast_kernel(FastParams p) {
     extern __shared__ __align__(512) uint8_t smem[];
     __shared__ uint8_t id_bin[64];
     __shared__ int fix_cols[kFastWarps][2][kFixList];
@@ -206,6 +207,11 @@ __global__ void __launch_bounds__(kFastWarps * 32) ldp_fast_kernel(FastParams p)
 
         auto load_raw = [&](int r) -> Raw {
             const uint8_t* rowp = img_px + int64_t(min(max(r, 0), p.rows - 1)) * p.pitch;
+            // pull a row further ahead into L2 so the register prefetch hits L2
+            if (sl == 1) {
+                const uint8_t* ahead = img_px + int64_t(min(max(r + kL2Ahead, 0), p.rows - 1)) * p.pitch + c0;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(ahead));
+            }
             Raw q;
             q.w = __ldg(reinterpret_cast<const uint2*>(rowp + own_off));
             q.h = halo_lane ? __ldg(reinterpret_cast<const uint32_t*>(rowp + halo_off)) : 0u;
@@ -261,40 +267,46 @@ __global__ void __launch_bounds__(kFastWarps * 32) ldp_fast_kernel(FastParams p)
         const bool any_hist = __any_sync(0xffffffffu, do_hist);
         const bool lane_out = seg_live && y < p.cols;
 
-        auto count = [&](const uint32_t (&X)[4]) {
+        // Slot addresses of the 8 pixel ids: pair q covers slots (lo, hi) =
+        // (q/2*4 + q%2, +2). The id sits in bits 0-5 (lo) and 16-21 (hi):
+        // lo offset = (X*4) & 0xFC, hi offset = (X >> 14) & 0xFC (the shift
+        // as a multiply-high so it issues on the FMA pipe, not the ALU).
+        auto addrs = [&](const uint32_t (&X)[4], uint32_t (&ad)[8]) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int s_lo = (q >> 1) * 4 + (q & 1), s_hi = s_lo + 2;
-                red_shared(((X[q] << 2) & 0xFCu) | slot[s_lo]);
-                red_shared(((X[q] >> 14) & 0xFCu) | slot[s_hi]);
+                ad[s_lo] = ((X[q] * 4u) & 0xFCu) | slot[s_lo];
+                ad[s_hi] = (__umulhi(X[q], 1u << 18) & 0xFCu) | slot[s_hi];
             }
         };
 
         auto step = [&](const Row8& a, const Row8& b, const Row8& c, int i) {
-            uint32_t X[4];
+            uint32_t X[4], ad[8];
             row_ids<K>(a, b, c, X);
+            addrs(X, ad);
             const bool live = i < seg_rows;
             if (dst) {
                 uint32_t e[8];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int s_lo = (q >> 1) * 4 + (q & 1), s_hi = s_lo + 2;
-                    e[s_lo] = lds32((((X[q] << 2) & 0xFCu) | slot[s_lo]) - 256);
-                    e[s_hi] = lds32((((X[q] >> 14) & 0xFCu) | slot[s_hi]) - 256);
-                }
-                const uint32_t w0 = prmt(prmt(e[0], e[1], 0x0040), prmt(e[2], e[3], 0x0040), 0x5410);
-                const uint32_t w1 = prmt(prmt(e[4], e[5], 0x0040), prmt(e[6], e[7], 0x0040), 0x5410);
+                for (int s = 0; s < 8; ++s) e[s] = lds32(ad[s] - 256);
+                // bytes -> words with multiply-adds (FMA pipe): code < 256
+                const uint32_t w0 = e[0] + e[1] * 0x100u + e[2] * 0x10000u + e[3] * 0x1000000u;
+                const uint32_t w1 = e[4] + e[5] * 0x100u + e[6] * 0x10000u + e[7] * 0x1000000u;
                 if (live && lane_out)
                     *reinterpret_cast<uint2*>(dst + int64_t(r0 + i) * p.codes_pitch + y) = make_uint2(w0, w1);
             }
             if (any_hist) {
                 if (CELLS && (i == 0 || i == p.cell_rows - 1)) {
                     // cell border row: count with the outside row clamped to the cell
-                    uint32_t Y[4];
+                    uint32_t Y[4], bd[8];
                     row_ids<K>(i == 0 ? b : a, b, i == p.cell_rows - 1 ? b : c, Y);
-                    if (live) count(Y);
+                    addrs(Y, bd);
+                    if (live)
+#pragma unroll
+                        for (int s = 0; s < 8; ++s) red_shared(bd[s]);
                 } else if (live) {
-                    count(X);
+#pragma unroll
+                    for (int s = 0; s < 8; ++s) red_shared(ad[s]);
                 }
             }
         };
