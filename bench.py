@@ -232,6 +232,7 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_1810_11518_b200 as aldp
+    from paper_1810_11518_b200.shard import gather_histograms, shard_range, wire_dtype_ok
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -244,7 +245,7 @@ def main():
     n, rows, cols, k, cr, cc, blobs, gen, seed = CONFIGS[args.config]
     if args.images:
         n = args.images
-    lo, hi = n * rank // world, n * (rank + 1) // world
+    lo, hi = shard_range(n, rank, world)
     mine = hi - lo
     pitch = cols  # 640/1024/16384: already 16-byte aligned
     stream = torch.cuda.Stream(dev)
@@ -268,7 +269,8 @@ def main():
         gathered = None
         if world > 1:
             # uint16 on the wire: a cell count is at most 81*91 = 7371 < 65536
-            per = [(n * (r + 1) // world - n * r // world) for r in range(world)]
+            assert wire_dtype_ok((cr or rows) * (cc or cols))
+            per = [shard_range(n, r, world)[1] - shard_range(n, r, world)[0] for r in range(world)]
             assert len(set(per)) == 1, "image count must divide evenly across ranks"
             wire = torch.empty((mine, cells, nb), dtype=torch.int16, device=dev)
             if rank == 0:
@@ -280,8 +282,7 @@ def main():
                        kernel=args.kernel, stream=sp)
         if world > 1:
             with torch.cuda.stream(stream):
-                wire.copy_(hist)  # u32 -> u16 (exact, see above)
-                dist.gather(wire, gathered if rank == 0 else None, dst=0)
+                gather_histograms(hist, dist, rank, world, wire=wire, out=gathered)
 
     # ---- warmup ----
     for _ in range(args.warmup):
@@ -305,8 +306,7 @@ def main():
         ev[2 * i + 1].record(stream)
         if world > 1:
             with torch.cuda.stream(stream):
-                wire.copy_(hist)
-                dist.gather(wire, gathered if rank == 0 else None, dst=0)
+                gather_histograms(hist, dist, rank, world, wire=wire, out=gathered)
     t_end.record(stream)
     torch.cuda.synchronize(dev)
     if world > 1:
