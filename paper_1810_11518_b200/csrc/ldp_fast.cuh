@@ -1,30 +1,31 @@
 // ldp_fast.cuh -- the packed sm_100a LDP kernel (product hot path).
 //
 // Work unit: a "tile" = one image band (band_rows rows; in cell mode one cell
-// row) x 128 columns. A warp runs two tiles at once, one per 16-lane
-// segment; each lane owns 8 adjacent columns (one 8-byte load per row) and
-// slides down the band with three unpacked rows in registers and three raw
-// rows in flight (software prefetch, distance 3).
+// row) x 128 columns. A tile is processed by a segment of 128/(4*NW) lanes;
+// each lane owns NW 4-byte words (4*NW adjacent columns) and slides down the
+// band with three unpacked rows in registers and three raw rows in flight
+// (software prefetch, distance 3) plus an L2 prefetch further ahead. NW = 1
+// (32-lane segments, one tile per warp, light registers -> high occupancy)
+// or NW = 2 (16-lane segments, two tiles per warp).
 //
-// Per lane and row, the 8 columns become four u16x2 pixel pairs with
-// stride-2 packing: word j (columns y+4j .. y+4j+3) gives A = (y+4j, y+4j+2)
-// and B = (y+4j+1, y+4j+3); the pair "P_A" has left/centre/right columns
-// (L, A, B) and "P_B" has (A, B, R), where L/R are A/B shifted by one column
-// (built with one byte permute from the neighbouring register; the segment
-// edges get their neighbour through a rotating shuffle and one halo load).
-// Pixel values are pre-scaled by 64 so every key K_i = 64*S_i + W[i] is one
-// 3-input add (ldp_common.cuh).
+// Per lane and row, each word becomes two u16x2 pixel pairs with stride-2
+// packing: word j (columns y+4j .. y+4j+3) gives A = (y+4j, y+4j+2) and
+// B = (y+4j+1, y+4j+3); pair "P_A" has left/centre/right columns (L, A, B),
+// pair "P_B" has (A, B, R), where L/R are A/B shifted by one column (one byte
+// permute from the neighbouring register; segment edges get their neighbour
+// through a rotating shuffle and one halo load). Pixel values are pre-scaled
+// by 64 so every key K_i = 64*S_i + W[i] is one 3-input add with its tag
+// (ldp_common.cuh).
 //
 // Histograms: per warp, per segment, one 64-entry u32 table per cell the
-// tile touches, counted by RED.shared.add (B200 serves same-address and
-// random-address shared reductions at ~1 warp-op/clk/SM -- measured, see
-// tools/microbench/atoms.cu -- so no replication is needed). Each table sits
-// 256 B after a private copy of the id->code table, so one address gives
-// both the code lookup (LDS [a-256]) and the count (RED [a]).
+// tile touches, counted by RED.shared.add (B200 serves same-address shared
+// reductions without serialisation -- measured, tools/microbench/atoms.cu).
+// Each table sits 256 B after a private copy of the id->code table, so one
+// address serves both the code lookup (LDS [a-256]) and the count (RED [a]).
 //
 // Cell mode (windowed_features semantics, every cell clamped as its own
-// image): the map always uses the whole-image clamp. Histogram counts differ
-// only on cell borders: the band's first/last row is recounted in the main
+// image): the map always uses the whole-image clamp; histogram counts differ
+// only on cell borders. The band's first/last row is recounted in the main
 // loop with the outside row replaced by the row itself; border columns are
 // masked out of the main count and recounted afterwards from clamped loads.
 #pragma once
@@ -32,18 +33,16 @@
 namespace aldp_b200 {
 
 constexpr int kFastWarps = 8;
-constexpr int kSegLanes = 16;
-constexpr int kLaneCols = 8;
-constexpr int kTileCols = kSegLanes * kLaneCols;  // 128
+constexpr int kTileCols = 128;
 constexpr int kMaxTileCells = 3;
 constexpr uint32_t kScaleMask = 0x3FC03FC0u;  // bytes 0 and 2 of a word, scaled by 64
-// Per-warp shared layout: for each segment kMaxTileCells regions + 1 trash
-// region; a region is [id->code table copy (256 B) | counts (256 B)].
+// Per-segment shared layout: kMaxTileCells regions + 1 trash region; a region
+// is [id->code table copy (256 B) | counts (256 B)].
 constexpr int kRegion = 512;
 constexpr int kSegRegions = kMaxTileCells + 1;
-constexpr int kWarpSmem = 2 * kSegRegions * kRegion;  // 4 KB
-constexpr int kFixList = 16;                           // fix columns per segment (max)
-constexpr int kL2Ahead = 12;                           // rows of L2 prefetch ahead of the load
+constexpr int kSegSmem = kSegRegions * kRegion;  // 2 KB
+constexpr int kFixList = 16;                      // border columns per segment (max)
+constexpr int kL2Ahead = 12;                      // rows of L2 prefetch ahead of the load
 
 struct FastParams {
     const uint8_t* px;
@@ -57,67 +56,73 @@ struct FastParams {
     int cell_rows, cell_cols, grid_r, grid_c;  // cell mode only
     int band_rows, bands, blocks;
     int64_t n_tiles;
+    uint32_t one;         // 1 at run time: multiplier that keeps integer adds on the FMA pipe
     uint8_t id_code[64];  // XOR id -> code (0 where no code has that id)
     uint8_t id_bin[64];   // XOR id -> histogram bin (colex rank of the code)
-};
-
-struct Raw {
-    uint2 w;     // columns y..y+7
-    uint32_t h;  // halo word (segment lane 15: left, lane 0: right)
-};
-
-// Unpacked row: pairs and their horizontal pair sums.
-struct Row8 {
-    uint32_t L0, A0, B0, R0, L1, A1, B1, R1;
-    uint32_t la0, ab0, br0, la1, ab1, br1;
 };
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
     return __byte_perm(a, b, s);
 }
 
-// Keys of one pixel pair from its left/centre/right column registers of rows
-// a (above), b, c (below) and the pair sums lc = l + c, cr = c + r. Ring:
-// TL=a.l T=a.c TR=a.r R=b.r BR=c.r B=c.c BL=c.l L=b.l (kirsch.cpp:11-12);
-// S_i = r[(2-i)&7] + r[(3-i)&7] + r[(4-i)&7].
+// Integer add issued as IMAD (FMA pipe) instead of IADD3 (ALU pipe): B200's
+// ALU pipe also runs every min/max of the selection network, so moving adds
+// off it raises throughput (tools/microbench/viadd.cu + ncu pipe counts:
+// IADD3 -> ALU, IMAD/VIADD -> FMA). `one` is 1 but unknown to the compiler.
+__device__ __forceinline__ uint32_t fadd(uint32_t a, uint32_t b, uint32_t one) {
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(one), "r"(b));
+    return r;
+}
+
+// Column registers of one pixel pair: left/centre/right and the pair sums
+// lc = l + c, cr = c + r (all scaled by 64).
 struct Col {
     uint32_t l, c, r, lc, cr;
 };
 
+// Keys of one pixel pair from rows a (above), b, c (below). Ring: TL=a.l
+// T=a.c TR=a.r R=b.r BR=c.r B=c.c BL=c.l L=b.l (kirsch.cpp:11-12);
+// S_i = r[(2-i)&7] + r[(3-i)&7] + r[(4-i)&7].
 template <int K>
-__device__ __forceinline__ uint32_t pair_id(const Col& a, const Col& b, const Col& c) {
+__device__ __forceinline__ uint32_t pair_id(const Col& a, const Col& b, const Col& c, uint32_t one) {
     constexpr uint32_t T0 = kTag(0) * 0x10001u, T1 = kTag(1) * 0x10001u, T2 = kTag(2) * 0x10001u,
                        T3 = kTag(3) * 0x10001u, T4 = kTag(4) * 0x10001u, T5 = kTag(5) * 0x10001u,
                        T6 = kTag(6) * 0x10001u, T7 = kTag(7) * 0x10001u;
     uint32_t k[8];
-    k[0] = a.r + b.r + c.r + T0;  // TR + R + BR
-    k[1] = a.cr + b.r + T1;       // T + TR + R
-    k[2] = a.lc + a.r + T2;       // TL + T + TR
-    k[3] = a.lc + b.l + T3;       // L + TL + T
-    k[4] = a.l + b.l + c.l + T4;  // BL + L + TL
-    k[5] = c.lc + b.l + T5;       // B + BL + L
-    k[6] = c.lc + c.r + T6;       // BR + B + BL
-    k[7] = c.cr + b.r + T7;       // R + BR + B
+    // all on the FMA pipe: IMAD for register adds, VIADD for the tags
+    k[0] = fadd(fadd(a.r, b.r, one), c.r, one) + T0;  // TR + R + BR
+    k[1] = fadd(a.cr, b.r, one) + T1;                  // T + TR + R
+    k[2] = fadd(a.lc, a.r, one) + T2;                  // TL + T + TR
+    k[3] = fadd(a.lc, b.l, one) + T3;                  // L + TL + T
+    k[4] = fadd(fadd(a.l, b.l, one), c.l, one) + T4;  // BL + L + TL
+    k[5] = fadd(c.lc, b.l, one) + T5;                  // B + BL + L
+    k[6] = fadd(c.lc, c.r, one) + T6;                  // BR + B + BL
+    k[7] = fadd(c.cr, b.r, one) + T7;                  // R + BR + B
     return topk_id<K>(k);
 }
 
-__device__ __forceinline__ Col colA(const Row8& r, int j) {  // pair P_A of word j
-    return j == 0 ? Col{r.L0, r.A0, r.B0, r.la0, r.ab0} : Col{r.L1, r.A1, r.B1, r.la1, r.ab1};
+// One unpacked row of a lane: per word j, A/B/L/R and the three pair sums.
+template <int NW>
+struct RowN {
+    uint32_t A[NW], B[NW], L[NW], R[NW];
+    uint32_t la[NW], ab[NW], br[NW];
+};
+
+template <int NW>
+__device__ __forceinline__ Col colA(const RowN<NW>& r, int j) {  // pair P_A of word j
+    return Col{r.L[j], r.A[j], r.B[j], r.la[j], r.ab[j]};
 }
-__device__ __forceinline__ Col colB(const Row8& r, int j) {  // pair P_B of word j
-    return j == 0 ? Col{r.A0, r.B0, r.R0, r.ab0, r.br0} : Col{r.A1, r.B1, r.R1, r.ab1, r.br1};
+template <int NW>
+__device__ __forceinline__ Col colB(const RowN<NW>& r, int j) {  // pair P_B of word j
+    return Col{r.A[j], r.B[j], r.R[j], r.ab[j], r.br[j]};
 }
 
-// ids of the lane's 8 pixels for output row b: X[0..3] = P_A(0), P_B(0),
-// P_A(1), P_B(1); each holds two 6-bit ids (bits 0-5 and 16-21).
-template <int K>
-__device__ __forceinline__ void row_ids(const Row8& a, const Row8& b, const Row8& c, uint32_t (&X)[4]) {
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        X[2 * j] = pair_id<K>(colA(a, j), colA(b, j), colA(c, j));
-        X[2 * j + 1] = pair_id<K>(colB(a, j), colB(b, j), colB(c, j));
-    }
-}
+template <int NW>
+struct RawN {
+    uint32_t w[NW];  // columns y .. y+4NW-1
+    uint32_t h;      // halo word (segment's last lane: left halo, lane 0: right halo)
+};
 
 __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
     uint32_t v;
@@ -128,23 +133,38 @@ __device__ __forceinline__ void red_shared(uint32_t addr) {
     asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr));
 }
 
-template <int K, bool CELLS>
-__global__ void __launch_bounds__(kFastWarps * 32, 2) ldp_fast_kernel(FastParams p) {
+template <int NW>
+__device__ __forceinline__ void load_words(const uint8_t* p, uint32_t (&w)[NW]) {
+    if constexpr (NW == 1) {
+        w[0] = __ldg(reinterpret_cast<const uint32_t*>(p));
+    } else {
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+        w[0] = v.x;
+        w[1] = v.y;
+    }
+}
+
+template <int K, int NW, bool CELLS, bool CODES, bool HIST>
+__global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_kernel(FastParams p) {
+    constexpr int LC = 4 * NW;              // columns per lane
+    constexpr int SEG = kTileCols / LC;     // lanes per segment (tile)
+    constexpr int NSEG = 32 / SEG;          // tiles per warp
+    constexpr int NPAIR = 2 * NW;           // u16x2 pixel pairs per lane
+    constexpr unsigned FULL = 0xffffffffu;
     extern __shared__ __align__(512) uint8_t smem[];
     __shared__ uint8_t id_bin[64];
-    __shared__ int fix_cols[kFastWarps][2][kFixList];
-    __shared__ int fix_n[kFastWarps][2];
+    __shared__ int fix_cols[kFastWarps][NSEG][kFixList];
+    __shared__ int fix_n[kFastWarps][NSEG];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int seg = lane >> 4, sl = lane & 15;
+    const int seg = lane / SEG, sl = lane % SEG;
     const uint32_t smem_base = uint32_t(__cvta_generic_to_shared(smem));
-    const uint32_t warp_base = smem_base + warp * kWarpSmem;
-    const uint32_t seg_base = warp_base + seg * kSegRegions * kRegion;
+    const uint32_t seg_base = smem_base + (warp * NSEG + seg) * kSegSmem;
 
     // id -> code table copies (one per region) and zeroed counts.
     {
         uint32_t* w = reinterpret_cast<uint32_t*>(smem);
-        const int words = kFastWarps * kWarpSmem / 4;
+        const int words = kFastWarps * NSEG * kSegSmem / 4;
         for (int i = threadIdx.x; i < words; i += blockDim.x) {
             const int in_region = i & (kRegion / 4 - 1);
             w[i] = in_region < 64 ? uint32_t(p.id_code[in_region]) : 0u;
@@ -156,12 +176,14 @@ __global__ void __launch_bounds__(kFastWarps * 32, 2) ldp_fast_kernel(FastParams
     const int64_t tiles_per_image = int64_t(p.bands) * p.blocks;
     const int64_t warp_global = int64_t(blockIdx.x) * kFastWarps + warp;
     const int64_t warp_stride = int64_t(gridDim.x) * kFastWarps;
-    const uint32_t src_prev = uint32_t((lane & 16) | ((lane + 15) & 15));
-    const uint32_t src_next = uint32_t((lane & 16) | ((lane + 1) & 15));
+    const uint32_t seg_lane0 = uint32_t(seg * SEG);
+    const uint32_t src_prev = seg_lane0 + uint32_t((sl + SEG - 1) % SEG);
+    const uint32_t src_next = seg_lane0 + uint32_t((sl + 1) % SEG);
     const uint32_t trash = seg_base + kMaxTileCells * kRegion + 256;
+    const uint32_t one = p.one;
 
-    for (int64_t pair = warp_global; 2 * pair < p.n_tiles; pair += warp_stride) {
-        const int64_t tile = 2 * pair + seg;
+    for (int64_t wt = warp_global; NSEG * wt < p.n_tiles; wt += warp_stride) {
+        const int64_t tile = NSEG * wt + seg;
         const bool seg_live = tile < p.n_tiles;
         const int64_t t = seg_live ? tile : p.n_tiles - 1;
         const int img = int(t / tiles_per_image);
@@ -169,89 +191,93 @@ __global__ void __launch_bounds__(kFastWarps * 32, 2) ldp_fast_kernel(FastParams
         const int band = rem / p.blocks, blk = rem - band * p.blocks;
         const int r0 = band * p.band_rows;
         const int seg_rows = seg_live ? min(p.rows, r0 + p.band_rows) - r0 : 0;
-        const int n_rows = max(seg_rows, __shfl_xor_sync(0xffffffffu, seg_rows, 16));
+        int n_rows = seg_rows;
+        if (NSEG > 1) n_rows = max(n_rows, __shfl_xor_sync(FULL, n_rows, 16));
         const int c0 = blk * kTileCols;
-        const int y = c0 + sl * kLaneCols;
+        const int y = c0 + sl * LC;
         const uint8_t* img_px = p.px + int64_t(img) * p.img_stride;
         const bool grid_band = !CELLS || band < p.grid_r;
-        const bool do_hist = p.hist != nullptr && seg_live && grid_band;
+        const bool do_hist = HIST && seg_live && grid_band;
 
         // ---- column clamp (image.cpp:36-40) as aligned offsets + selectors ----
         const int last = p.cols - 1;
         int halo_off;
         uint32_t halo_sel;
         {
-            const int col = sl == 15 ? c0 - 4 : c0 + kTileCols;
+            const int col = sl == SEG - 1 ? c0 - 4 : c0 + kTileCols;
             const int a = min(max(col, 0), last & ~3);
             halo_off = a;
             halo_sel = 0;
 #pragma unroll
             for (int j = 0; j < 4; ++j) halo_sel |= uint32_t(min(max(col + j, 0), last) - a) << (4 * j);
         }
-        const bool halo_lane = sl == 0 || sl == 15;
-        const uint32_t halo_rot = sl == 15 ? 30u : 6u;  // B form (bytes 1,3) / A form (bytes 0,2)
-        // Own 8 columns come from one aligned 8-byte window; a tile crossing
-        // the right image edge selects bytes so columns past it repeat the
-        // last pixel (warp-uniform branch; never taken for widths % 128 == 0).
-        const bool any_edge = __any_sync(0xffffffffu, c0 + kTileCols > p.cols);
-        const int own_off = min(y, last & ~7);
-        uint32_t sel0 = 0x3210u, sel1 = 0x7654u;
-        if (any_edge) {
-            sel0 = sel1 = 0;
+        const bool halo_lane = sl == 0 || sl == SEG - 1;
+        const uint32_t halo_rot = sl == SEG - 1 ? 30u : 6u;  // B form (bytes 1,3) / A form (bytes 0,2)
+        // Own columns come from one aligned window of 4*NW bytes; a tile
+        // crossing the right image edge selects bytes so columns past it
+        // repeat the last pixel (warp-uniform branch; never taken when the
+        // width is a multiple of 128).
+        const bool any_edge = __any_sync(FULL, c0 + kTileCols > p.cols);
+        const int own_off = min(y, last & ~(LC - 1));
+        uint32_t sel[NW];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                sel0 |= uint32_t(min(y + j, last) - own_off) << (4 * j);
-                sel1 |= uint32_t(min(y + 4 + j, last) - own_off) << (4 * j);
+        for (int j = 0; j < NW; ++j) sel[j] = 0x3210u + 0x4444u * j;
+        if (any_edge) {
+#pragma unroll
+            for (int j = 0; j < NW; ++j) {
+                sel[j] = 0;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) sel[j] |= uint32_t(min(y + 4 * j + b, last) - own_off) << (4 * b);
             }
         }
 
-        auto load_raw = [&](int r) -> Raw {
+        auto load_raw = [&](int r) -> RawN<NW> {
             const uint8_t* rowp = img_px + int64_t(min(max(r, 0), p.rows - 1)) * p.pitch;
-            // pull a row further ahead into L2 so the register prefetch hits L2
-            if (sl == 1) {
+            if (sl == 1) {  // pull a row further ahead into L2
                 const uint8_t* ahead = img_px + int64_t(min(max(r + kL2Ahead, 0), p.rows - 1)) * p.pitch + c0;
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(ahead));
             }
-            Raw q;
-            q.w = __ldg(reinterpret_cast<const uint2*>(rowp + own_off));
+            RawN<NW> q;
+            load_words<NW>(rowp + own_off, q.w);
             q.h = halo_lane ? __ldg(reinterpret_cast<const uint32_t*>(rowp + halo_off)) : 0u;
             return q;
         };
-        auto unpack = [&](const Raw& q) -> Row8 {
-            uint32_t w0 = q.w.x, w1 = q.w.y;
+        auto unpack = [&](const RawN<NW>& q) -> RowN<NW> {
+            uint32_t w[NW];
+#pragma unroll
+            for (int j = 0; j < NW; ++j) w[j] = q.w[j];
             if (any_edge) {
-                w0 = prmt(q.w.x, q.w.y, sel0);
-                w1 = prmt(q.w.x, q.w.y, sel1);
+#pragma unroll
+                for (int j = 0; j < NW; ++j) w[j] = prmt(q.w[0], q.w[NW - 1], NW == 1 ? sel[j] & 0x3333u : sel[j]);
             }
             const uint32_t hv = prmt(q.h, q.h, halo_sel);
             const uint32_t h = __funnelshift_l(hv, hv, halo_rot) & kScaleMask;
-            Row8 r;
-            r.A0 = (w0 << 6) & kScaleMask;
-            r.B0 = (w0 >> 2) & kScaleMask;
-            r.A1 = (w1 << 6) & kScaleMask;
-            r.B1 = (w1 >> 2) & kScaleMask;
-            const uint32_t xb = sl == 15 ? h : r.B1;
-            const uint32_t ya = sl == 0 ? h : r.A0;
-            const uint32_t prevB = __shfl_sync(0xffffffffu, xb, src_prev);
-            const uint32_t nextA = __shfl_sync(0xffffffffu, ya, src_next);
-            r.L0 = prmt(r.B0, prevB, 0x1076);  // (y-1, y+1)
-            r.R0 = prmt(r.A0, r.A1, 0x5432);   // (y+2, y+4)
-            r.L1 = prmt(r.B1, r.B0, 0x1076);   // (y+3, y+5)
-            r.R1 = prmt(r.A1, nextA, 0x5432);  // (y+6, y+8)
-            r.la0 = r.L0 + r.A0;
-            r.ab0 = r.A0 + r.B0;
-            r.br0 = r.B0 + r.R0;
-            r.la1 = r.L1 + r.A1;
-            r.ab1 = r.A1 + r.B1;
-            r.br1 = r.B1 + r.R1;
+            RowN<NW> r;
+#pragma unroll
+            for (int j = 0; j < NW; ++j) {
+                r.A[j] = (w[j] << 6) & kScaleMask;
+                r.B[j] = (w[j] >> 2) & kScaleMask;
+            }
+            const uint32_t xb = sl == SEG - 1 ? h : r.B[NW - 1];
+            const uint32_t ya = sl == 0 ? h : r.A[0];
+            const uint32_t prevB = __shfl_sync(FULL, xb, src_prev);
+            const uint32_t nextA = __shfl_sync(FULL, ya, src_next);
+#pragma unroll
+            for (int j = 0; j < NW; ++j) {
+                r.L[j] = prmt(r.B[j], j == 0 ? prevB : r.B[j - 1], 0x1076);       // (y+4j-1, y+4j+1)
+                r.R[j] = prmt(r.A[j], j == NW - 1 ? nextA : r.A[j + 1], 0x5432);  // (y+4j+2, y+4j+4)
+                r.la[j] = fadd(r.L[j], r.A[j], one);
+                r.ab[j] = fadd(r.A[j], r.B[j], one);
+                r.br[j] = fadd(r.B[j], r.R[j], one);
+            }
             return r;
         };
 
         // ---- histogram slots: region address per pixel (or trash) ----
         const int cell_c0 = CELLS ? c0 / p.cell_cols : 0;
-        uint32_t slot[8];
+        uint32_t slot[LC];
 #pragma unroll
-        for (int s = 0; s < 8; ++s) {
+        for (int s = 0; s < LC; ++s) {
             const int col = y + s;
             bool on = do_hist && col < p.cols;
             int lc = 0;
@@ -262,60 +288,68 @@ __global__ void __launch_bounds__(kFastWarps * 32, 2) ldp_fast_kernel(FastParams
             }
             slot[s] = on ? seg_base + uint32_t(lc) * kRegion + 256 : trash;
         }
-        // map slots of the four pairs: P_A(0) lo/hi = 0/2, P_B(0) = 1/3, P_A(1) = 4/6, P_B(1) = 5/7
-        uint8_t* dst = p.codes ? p.codes + int64_t(img) * p.codes_img_stride : nullptr;
-        const bool any_hist = __any_sync(0xffffffffu, do_hist);
+        uint8_t* dst = CODES ? p.codes + int64_t(img) * p.codes_img_stride : nullptr;
         const bool lane_out = seg_live && y < p.cols;
 
-        // Slot addresses of the 8 pixel ids: pair q covers slots (lo, hi) =
-        // (q/2*4 + q%2, +2). The id sits in bits 0-5 (lo) and 16-21 (hi):
-        // lo offset = (X*4) & 0xFC, hi offset = (X >> 14) & 0xFC (the shift
-        // as a multiply-high so it issues on the FMA pipe, not the ALU).
-        auto addrs = [&](const uint32_t (&X)[4], uint32_t (&ad)[8]) {
+        // Slot addresses of the lane's pixel ids. Pair q = 2j (P_A of word
+        // j) covers columns y+4j (lo) / y+4j+2 (hi); q = 2j+1 (P_B) covers
+        // y+4j+1 / y+4j+3. The id sits in bits 0-5 (lo) and 16-21 (hi).
+        auto addrs = [&](const uint32_t (&X)[NPAIR], uint32_t (&ad)[LC]) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < NPAIR; ++q) {
                 const int s_lo = (q >> 1) * 4 + (q & 1), s_hi = s_lo + 2;
                 ad[s_lo] = ((X[q] * 4u) & 0xFCu) | slot[s_lo];
                 ad[s_hi] = (__umulhi(X[q], 1u << 18) & 0xFCu) | slot[s_hi];
             }
         };
+        auto row_ids = [&](const RowN<NW>& a, const RowN<NW>& b, const RowN<NW>& c, uint32_t (&X)[NPAIR]) {
+#pragma unroll
+            for (int j = 0; j < NW; ++j) {
+                X[2 * j] = pair_id<K>(colA(a, j), colA(b, j), colA(c, j), one);
+                X[2 * j + 1] = pair_id<K>(colB(a, j), colB(b, j), colB(c, j), one);
+            }
+        };
 
-        auto step = [&](const Row8& a, const Row8& b, const Row8& c, int i) {
-            uint32_t X[4], ad[8];
-            row_ids<K>(a, b, c, X);
+        auto step = [&](const RowN<NW>& a, const RowN<NW>& b, const RowN<NW>& c, int i) {
+            uint32_t X[NPAIR], ad[LC];
+            row_ids(a, b, c, X);
             addrs(X, ad);
             const bool live = i < seg_rows;
-            if (dst) {
-                uint32_t e[8];
+            if (CODES) {
+                uint32_t e[LC];
 #pragma unroll
-                for (int s = 0; s < 8; ++s) e[s] = lds32(ad[s] - 256);
-                // bytes -> words with multiply-adds (FMA pipe): code < 256
-                const uint32_t w0 = e[0] + e[1] * 0x100u + e[2] * 0x10000u + e[3] * 0x1000000u;
-                const uint32_t w1 = e[4] + e[5] * 0x100u + e[6] * 0x10000u + e[7] * 0x1000000u;
-                if (live && lane_out)
-                    *reinterpret_cast<uint2*>(dst + int64_t(r0 + i) * p.codes_pitch + y) = make_uint2(w0, w1);
+                for (int s = 0; s < LC; ++s) e[s] = lds32(ad[s] - 256);
+                uint32_t wd[NW];
+#pragma unroll
+                for (int j = 0; j < NW; ++j)  // bytes -> word with multiply-adds (FMA pipe)
+                    wd[j] = e[4 * j] + e[4 * j + 1] * 0x100u + e[4 * j + 2] * 0x10000u + e[4 * j + 3] * 0x1000000u;
+                if (live && lane_out) {
+                    uint8_t* o = dst + int64_t(r0 + i) * p.codes_pitch + y;
+                    if constexpr (NW == 1) *reinterpret_cast<uint32_t*>(o) = wd[0];
+                    else *reinterpret_cast<uint2*>(o) = make_uint2(wd[0], wd[1]);
+                }
             }
-            if (any_hist) {
+            if (HIST) {
                 if (CELLS && (i == 0 || i == p.cell_rows - 1)) {
                     // cell border row: count with the outside row clamped to the cell
-                    uint32_t Y[4], bd[8];
-                    row_ids<K>(i == 0 ? b : a, b, i == p.cell_rows - 1 ? b : c, Y);
+                    uint32_t Y[NPAIR], bd[LC];
+                    row_ids(i == 0 ? b : a, b, i == p.cell_rows - 1 ? b : c, Y);
                     addrs(Y, bd);
                     if (live)
 #pragma unroll
-                        for (int s = 0; s < 8; ++s) red_shared(bd[s]);
+                        for (int s = 0; s < LC; ++s) red_shared(bd[s]);
                 } else if (live) {
 #pragma unroll
-                    for (int s = 0; s < 8; ++s) red_shared(ad[s]);
+                    for (int s = 0; s < LC; ++s) red_shared(ad[s]);
                 }
             }
         };
 
         // ---- main loop: rows r0 .. r0+n_rows-1, unrolled by 3 ----
-        Row8 ra = unpack(load_raw(r0 - 1));
-        Row8 rb = unpack(load_raw(r0));
-        Row8 rc = unpack(load_raw(r0 + 1));
-        Raw q0 = load_raw(r0 + 2), q1 = load_raw(r0 + 3), q2 = load_raw(r0 + 4);
+        RowN<NW> ra = unpack(load_raw(r0 - 1));
+        RowN<NW> rb = unpack(load_raw(r0));
+        RowN<NW> rc = unpack(load_raw(r0 + 1));
+        RawN<NW> q0 = load_raw(r0 + 2), q1 = load_raw(r0 + 3), q2 = load_raw(r0 + 4);
         for (int i = 0; i < n_rows; i += 3) {
             step(ra, rb, rc, i);
             if (i + 1 >= n_rows) break;
@@ -332,7 +366,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, 2) ldp_fast_kernel(FastParams
         }
 
         // ---- cell border columns: recount with the cell clamp ----
-        if (CELLS && __any_sync(0xffffffffu, do_hist)) {
+        if (HIST && CELLS && __any_sync(FULL, do_hist)) {
             int* fl = fix_cols[warp][seg];
             if (sl == 0) {
                 int n = 0;
@@ -347,50 +381,96 @@ __global__ void __launch_bounds__(kFastWarps * 32, 2) ldp_fast_kernel(FastParams
                 fix_n[warp][seg] = n;
             }
             __syncwarp();
-            const int items = fix_n[warp][seg] * seg_rows;
-            const int max_items = max(items, __shfl_xor_sync(0xffffffffu, items, 16));
+            // Vertical runs: the segment's 2*SEG u16 half-slots split the
+            // border columns x rows; each slot slides down one column with a
+            // 3-row window of the bytes (col-1, col, col+1), clamped to the cell
+            // (rows to the band = cell row, the outside column to the column).
+            const int nb = fix_n[warp][seg];
+            const int runs_per_col = nb ? max(1, (2 * SEG) / nb) : 1;
+            const int run_len = nb ? (seg_rows + runs_per_col - 1) / runs_per_col : 0;
             const int x_lo = r0, x_hi = r0 + p.cell_rows - 1;
-            for (int base = 0; base < max_items; base += 2 * kSegLanes) {
-                // two border pixels per lane, one per u16x2 half
-                uint32_t rv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                uint32_t addr[2] = {trash, trash};
+            int xs[2], len[2];
+            uint32_t wsel[2], addr[2];
+            const uint8_t* colp[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int sidx = sl + SEG * h;
+                const int ci = sidx / runs_per_col, ri = sidx - ci * runs_per_col;
+                const bool act = ci < nb && ri * run_len < seg_rows;
+                const int col = act ? fl[ci] : y;
+                const int cc = col / max(p.cell_cols, 1);
+                const bool left = col == cc * p.cell_cols;
+                xs[h] = r0 + ri * run_len;
+                len[h] = act ? min(run_len, seg_rows - ri * run_len) : 0;
+                const int wo = max(col - 1, 0) & ~3;
+                colp[h] = img_px + wo;
+                // byte offset of column col-1 inside the 8-byte window at wo;
+                // left border: (c, c, r); right border: (l, c, c)
+                const uint32_t o = uint32_t(col - 1 - wo);
+                wsel[h] = left ? (o + 1) | ((o + 1) << 4) | ((o + 2) << 8) : o | ((o + 1) << 4) | ((o + 1) << 8);
+                addr[h] = act ? seg_base + uint32_t(cc - cell_c0) * kRegion + 256 : trash;
+            }
+            int n_it = max(len[0], len[1]);
+            for (int o = 16; o > 0; o >>= 1) n_it = max(n_it, __shfl_xor_sync(FULL, n_it, o));
+            // raw 8-byte windows of one row for both halves (the second word
+            // only when it holds column col+1 -- it never leaves the row)
+            bool need_hi[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) need_hi[h] = ((wsel[h] >> 8) & 0xFu) >= 4u;
+            auto fetch = [&](int rh0, int rh1, uint32_t (&q)[4]) {
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    const int it = base + sl + kSegLanes * h;
-                    if (it >= items) continue;
-                    const int col = fl[it / seg_rows];
-                    const int x = r0 + it % seg_rows;
-                    const int cc = col / p.cell_cols;
-                    const int y_lo = cc * p.cell_cols, y_hi = y_lo + p.cell_cols - 1;
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        const int xx = min(max(x + ring_dx(q), x_lo), x_hi);
-                        const int yy = min(max(col + ring_dy(q), y_lo), y_hi);
-                        rv[q] |= uint32_t(__ldg(img_px + int64_t(xx) * p.pitch + yy)) << (16 * h + 6);
-                    }
-                    addr[h] = seg_base + uint32_t(cc - cell_c0) * kRegion + 256;
+                    const int rr = min(max(h == 0 ? rh0 : rh1, x_lo), x_hi);
+                    const uint8_t* ptr = colp[h] + int64_t(rr) * p.pitch;
+                    q[2 * h] = __ldg(reinterpret_cast<const uint32_t*>(ptr));
+                    q[2 * h + 1] = need_hi[h] ? __ldg(reinterpret_cast<const uint32_t*>(ptr + 4)) : 0u;
                 }
-                // ring slots: 0 TL, 1 T, 2 TR, 3 R, 4 BR, 5 B, 6 BL, 7 L
-                const Col a{rv[0], rv[1], rv[2], rv[0] + rv[1], rv[1] + rv[2]};
-                const Col b{rv[7], 0u, rv[3], 0u, 0u};
-                const Col c{rv[6], rv[5], rv[4], rv[6] + rv[5], rv[5] + rv[4]};
-                const uint32_t X = pair_id<K>(a, b, c);
-                red_shared(((X << 2) & 0xFCu) | addr[0]);
-                red_shared(((X >> 14) & 0xFCu) | addr[1]);
+            };
+            // packed u16x2 (l, c, r) x64 of one row from its raw windows
+            auto make_col = [&](const uint32_t (&q)[4]) -> Col {
+                const uint32_t w0 = prmt(q[0], q[1], wsel[0]) & 0x00FFFFFFu;
+                const uint32_t w1 = prmt(q[2], q[3], wsel[1]) & 0x00FFFFFFu;
+                Col c;
+                c.l = prmt(w0, w1, 0x7430) << 6;
+                c.c = prmt(w0, w1, 0x7531) << 6;
+                c.r = prmt(w0, w1, 0x7632) << 6;
+                c.lc = fadd(c.l, c.c, one);
+                c.cr = fadd(c.c, c.r, one);
+                return c;
+            };
+            uint32_t qa[4], qb[4], qn[4];
+            fetch(xs[0] - 1, xs[1] - 1, qa);
+            fetch(xs[0], xs[1], qb);
+            fetch(xs[0] + 1, xs[1] + 1, qn);
+            Col wa = make_col(qa), wb = make_col(qb);
+            for (int it = 0; it < n_it; ++it) {
+                const Col wc = make_col(qn);
+                fetch(xs[0] + it + 2, xs[1] + it + 2, qn);  // next row in flight
+                const uint32_t X = pair_id<K>(wa, wb, wc, one);
+                red_shared(((X * 4u) & 0xFCu) | (it < len[0] ? addr[0] : trash));
+                red_shared((__umulhi(X, 1u << 18) & 0xFCu) | (it < len[1] ? addr[1] : trash));
+                wa = wb;
+                wb = wc;
             }
         }
         __syncwarp();
 
         // ---- flush: one global atomic per (cell, bin) seen, then re-zero ----
-        if (p.hist != nullptr) {
-            const int ntab = !do_hist ? 0 : CELLS ? min(c0 + kTileCols, min(p.cols, p.grid_c * p.cell_cols)) > c0
-                                                       ? (min(c0 + kTileCols, min(p.cols, p.grid_c * p.cell_cols)) - 1) / p.cell_cols - cell_c0 + 1
-                                                       : 0
-                                                 : 1;
+        if (HIST) {
+            int ntab = 0;
+            if (do_hist) {
+                if (CELLS) {
+                    const int c_end = min(c0 + kTileCols, min(p.cols, p.grid_c * p.cell_cols));
+                    ntab = c_end > c0 ? (c_end - 1) / p.cell_cols - cell_c0 + 1 : 0;
+                } else {
+                    ntab = 1;
+                }
+            }
             const int64_t cells_per_image = CELLS ? int64_t(p.grid_r) * p.grid_c : 1;
-            for (int j = sl; j < ntab * 64; j += kSegLanes) {
+            uint8_t* seg_ptr = smem + (seg_base - smem_base);
+            for (int j = sl; j < ntab * 64; j += SEG) {
                 const int lc = j >> 6, id = j & 63;
-                uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + (seg_base - smem_base) + lc * kRegion + 256);
+                uint32_t* cnt = reinterpret_cast<uint32_t*>(seg_ptr + lc * kRegion + 256);
                 const uint32_t v = cnt[id];
                 if (v) {
                     const int64_t cell = CELLS ? int64_t(band) * p.grid_c + cell_c0 + lc : 0;
@@ -398,9 +478,9 @@ __global__ void __launch_bounds__(kFastWarps * 32, 2) ldp_fast_kernel(FastParams
                     cnt[id] = 0;
                 }
             }
-            // the trash region may have collected counts: clear it too
-            uint32_t* tr = reinterpret_cast<uint32_t*>(smem + (trash - smem_base));
-            for (int j = sl; j < 64; j += kSegLanes) tr[j] = 0;
+            // the trash region collects masked counts: clear it too
+            uint32_t* tr = reinterpret_cast<uint32_t*>(seg_ptr + kMaxTileCells * kRegion + 256);
+            for (int j = sl; j < 64; j += SEG) tr[j] = 0;
         }
         __syncwarp();
     }

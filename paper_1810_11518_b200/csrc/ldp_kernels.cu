@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -122,44 +123,67 @@ static int n_sms() {
     return cache[dev];
 }
 
-template <int K, bool CELLS>
+template <int K, int NW, bool CELLS, bool CODES, bool HIST>
 static aldp_status launch_fast_t(const FastParams& p, cudaStream_t st) {
-    const size_t smem = size_t(kFastWarps) * kWarpSmem;
+    auto kern = ldp_fast_kernel<K, NW, CELLS, CODES, HIST>;
+    constexpr int NSEG = 32 / (kTileCols / (4 * NW));
+    const size_t smem = size_t(kFastWarps) * NSEG * kSegSmem;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
+    static int per_sm = 1;
     std::call_once(once, [&] {
-        attr_err = cudaFuncSetAttribute(ldp_fast_kernel<K, CELLS>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (attr_err == cudaSuccess)
+            attr_err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFastWarps * 32, smem);
+        if (per_sm < 1) per_sm = 1;
     });
-    if (attr_err != cudaSuccess) return cuda_fail(attr_err, "cudaFuncSetAttribute");
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ldp_fast_kernel<K, CELLS>, kFastWarps * 32,
-                                                  smem);
-    if (per_sm < 1) per_sm = 1;
-    const int64_t pairs = (p.n_tiles + 1) / 2;
-    const int64_t want = (pairs + kFastWarps - 1) / kFastWarps;
+    if (attr_err != cudaSuccess) return cuda_fail(attr_err, "fast kernel setup");
+    const int64_t warp_tiles = (p.n_tiles + NSEG - 1) / NSEG;
+    const int64_t want = (warp_tiles + kFastWarps - 1) / kFastWarps;
     const int grid = int(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(per_sm) * n_sms())));
-    ldp_fast_kernel<K, CELLS><<<grid, kFastWarps * 32, smem, st>>>(p);
+    kern<<<grid, kFastWarps * 32, smem, st>>>(p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "ldp_fast_kernel launch");
     return ALDP_OK;
 }
 
-template <int K>
-static aldp_status launch_fast_k(const FastParams& p, bool cells, cudaStream_t st) {
-    return cells ? launch_fast_t<K, true>(p, st) : launch_fast_t<K, false>(p, st);
+template <int K, int NW>
+static aldp_status launch_fast_kw(const FastParams& p, bool cells, cudaStream_t st) {
+    const bool codes = p.codes != nullptr, hist = p.hist != nullptr;
+    if (cells) {  // cell geometry only matters for histograms
+        return codes ? launch_fast_t<K, NW, true, true, true>(p, st)
+                     : launch_fast_t<K, NW, true, false, true>(p, st);
+    }
+    if (codes && hist) return launch_fast_t<K, NW, false, true, true>(p, st);
+    if (codes) return launch_fast_t<K, NW, false, true, false>(p, st);
+    return launch_fast_t<K, NW, false, false, true>(p, st);
 }
 
-static aldp_status launch_fast(const FastParams& p, int k, bool cells, cudaStream_t st) {
+template <int K>
+static aldp_status launch_fast_k(const FastParams& p, bool cells, int nw, cudaStream_t st) {
+    return nw == 2 ? launch_fast_kw<K, 2>(p, cells, st) : launch_fast_kw<K, 1>(p, cells, st);
+}
+
+static aldp_status launch_fast(const FastParams& p, int k, bool cells, int nw, cudaStream_t st) {
     switch (k) {
-    case 1: return launch_fast_k<1>(p, cells, st);
-    case 2: return launch_fast_k<2>(p, cells, st);
-    case 3: return launch_fast_k<3>(p, cells, st);
-    case 5: return launch_fast_k<5>(p, cells, st);
-    case 6: return launch_fast_k<6>(p, cells, st);
-    case 7: return launch_fast_k<7>(p, cells, st);
+    case 1: return launch_fast_k<1>(p, cells, nw, st);
+    case 2: return launch_fast_k<2>(p, cells, nw, st);
+    case 3: return launch_fast_k<3>(p, cells, nw, st);
+    case 5: return launch_fast_k<5>(p, cells, nw, st);
+    case 6: return launch_fast_k<6>(p, cells, nw, st);
+    case 7: return launch_fast_k<7>(p, cells, nw, st);
     default: return fail(ALDP_EINVAL, "fast kernel: unsupported k");
     }
+}
+
+// Words (4-byte column groups) per lane of the fast kernel: 2 (default) or 1.
+// ALDP_LANE_WORDS overrides it for experiments.
+static int lane_words() {
+    static const int nw = [] {
+        const char* e = std::getenv("ALDP_LANE_WORDS");
+        return (e && std::atoi(e) == 1) ? 1 : 2;
+    }();
+    return nw;
 }
 
 // Most cells a 128-column tile can touch for this geometry.
@@ -211,16 +235,18 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
                                       sizeof(uint32_t) * size_t(a->n_images) * cells * nbins, st));
     if (a->n_images == 0 || (!a->d_codes && !a->d_hist)) return ALDP_OK;
 
+    const int nw = lane_words();
+    const int al = 4 * nw;  // alignment the per-lane vector loads/stores need
     const bool aligned =
-        a->cols % 4 == 0 && a->pitch % 8 == 0 && (a->n_images <= 1 || a->img_stride % 8 == 0) &&
-        (reinterpret_cast<uintptr_t>(a->d_pixels) & 7) == 0 &&
-        (!a->d_codes || (a->codes_pitch % 8 == 0 && (reinterpret_cast<uintptr_t>(a->d_codes) & 7) == 0 &&
-                         (a->n_images <= 1 || a->codes_img_stride % 8 == 0)));
+        a->cols % 4 == 0 && a->pitch % al == 0 && (a->n_images <= 1 || a->img_stride % al == 0) &&
+        (reinterpret_cast<uintptr_t>(a->d_pixels) % al) == 0 &&
+        (!a->d_codes || (a->codes_pitch % al == 0 && (reinterpret_cast<uintptr_t>(a->d_codes) % al) == 0 &&
+                         (a->n_images <= 1 || a->codes_img_stride % al == 0)));
     int ncl = 1;
     if (a->cell_rows) ncl = max_cells_per_tile(a->cols, a->cell_cols, grid_c);
     const bool fast_ok = aligned && a->k != 4 && ncl <= kMaxTileCells;
     if (kernel == ALDP_KERNEL_FAST && !fast_ok)
-        return fail(ALDP_EINVAL, "fast kernel needs cols % 4 == 0, pitches/strides % 8 == 0, "
+        return fail(ALDP_EINVAL, "fast kernel needs cols % 4 == 0, aligned pitches/strides, "
                                  "k != 4 and at most 3 cells per 128 columns");
     if (kernel != ALDP_KERNEL_GENERIC && fast_ok) {
         FastParams p{};
@@ -243,13 +269,14 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
         p.bands = (a->rows + p.band_rows - 1) / p.band_rows;
         p.blocks = (a->cols + kTileCols - 1) / kTileCols;
         p.n_tiles = int64_t(a->n_images) * p.bands * p.blocks;
+        p.one = 1;
         for (int id = 0; id < 64; ++id) p.id_code[id] = p.id_bin[id] = 0;
         for (int c = 0; c < 256; ++c)
             if (popcount8(c) == a->k) {
                 p.id_code[tag_xor(c)] = uint8_t(c);
                 p.id_bin[tag_xor(c)] = uint8_t(colex_rank(c));
             }
-        return launch_fast(p, a->k, a->cell_rows != 0, st);
+        return launch_fast(p, a->k, a->cell_rows != 0 && a->d_hist != nullptr, nw, st);
     }
     GenericParams g{};
     g.px = a->d_pixels;

@@ -22,6 +22,11 @@ __device__ __forceinline__ unsigned op(int k, unsigned a, unsigned b) {
     case 9: asm volatile("shf.l.wrap.b32 %0, %1, %2, 6;" : "=r"(r) : "r"(a), "r"(b)); break;  // SHF
     case 10: asm volatile("min.u16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b)); break;
     case 11: asm volatile("max.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b)); break;            // IMNMX
+    case 12: asm volatile("add.u32 %0, %1, 0x350035;" : "=r"(r) : "r"(a)); r ^= b & 0; break;    // VIADD imm
+    case 13: { unsigned t; asm volatile("add.u32 %0, %1, %2;" : "=r"(t) : "r"(a), "r"(b)); asm volatile("add.u32 %0, %1, 0x10001;" : "=r"(r) : "r"(t)); } break; // IADD3 3-in
+    case 14: asm volatile("mad.lo.u32 %0, %1, %3, %2;" : "=r"(r) : "r"(a), "r"(b), "r"(b >> 31 | 1u)); break; // IMAD x*reg+y
+    case 15: asm volatile("xor.b32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b)); break;             // LOP3
+    case 16: asm volatile("mul.hi.u32 %0, %1, 0x40000;" : "=r"(r) : "r"(a)); r ^= b & 0; break; // IMAD.HI
     default: r = a;
     }
     return r;
@@ -87,5 +92,14 @@ int main() {
     run("HMNMX2 + IMAD", probe<2, 1>);
     run("HMNMX2 + HADD2", probe<2, 3>);
     run("max+min u16x2", probe<0, 10>);
+    run("VIADD imm", probe<12, 12>);
+    run("VIADD + VIMNMX", probe<12, 0>);
+    run("VIADD + IMAD", probe<12, 1>);
+    run("IADD3 3-in", probe<13, 13>);
+    run("IADD3 + VIMNMX", probe<13, 0>);
+    run("IMAD reg-1", probe<14, 14>);
+    run("IMAD reg-1 + VIMNMX", probe<14, 0>);
+    run("IMAD.HI + VIMNMX", probe<16, 0>);
+    run("XOR + IMAD", probe<15, 1>);
     return 0;
 }
