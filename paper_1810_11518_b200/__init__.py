@@ -38,7 +38,8 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libaldp_b200.so")
+# ALDP_LIB points at an alternative build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("ALDP_LIB") or os.path.join(_HERE, "libaldp_b200.so")
 
 
 class ResponsePath(enum.IntEnum):

@@ -90,15 +90,34 @@ __device__ __forceinline__ uint32_t pair_id(const Col& a, const Col& b, const Co
                        T3 = kTag(3) * 0x10001u, T4 = kTag(4) * 0x10001u, T5 = kTag(5) * 0x10001u,
                        T6 = kTag(6) * 0x10001u, T7 = kTag(7) * 0x10001u;
     uint32_t k[8];
-    // all on the FMA pipe: IMAD for register adds, VIADD for the tags
-    k[0] = fadd(fadd(a.r, b.r, one), c.r, one) + T0;  // TR + R + BR
-    k[1] = fadd(a.cr, b.r, one) + T1;                  // T + TR + R
-    k[2] = fadd(a.lc, a.r, one) + T2;                  // TL + T + TR
-    k[3] = fadd(a.lc, b.l, one) + T3;                  // L + TL + T
-    k[4] = fadd(fadd(a.l, b.l, one), c.l, one) + T4;  // BL + L + TL
-    k[5] = fadd(c.lc, b.l, one) + T5;                  // B + BL + L
-    k[6] = fadd(c.lc, c.r, one) + T6;                  // BR + B + BL
-    k[7] = fadd(c.cr, b.r, one) + T7;                  // R + BR + B
+    // Pipe balance: the 3-input keys k0/k4 go to the FMA pipe (IMAD + VIADD),
+    // the 2-input keys to the ALU as one IADD3 each (ALDP_KEYMODE: 0 all
+    // IADD3, 1 this hybrid, 2 all FMA).
+#ifndef ALDP_KEYMODE
+#define ALDP_KEYMODE 1
+#endif
+    if constexpr (ALDP_KEYMODE == 0) {
+        k[0] = a.r + b.r + c.r + T0;
+        k[4] = a.l + b.l + c.l + T4;
+    } else {
+        k[0] = fadd(fadd(a.r, b.r, one), c.r, one) + T0;  // TR + R + BR
+        k[4] = fadd(fadd(a.l, b.l, one), c.l, one) + T4;  // BL + L + TL
+    }
+    if constexpr (ALDP_KEYMODE == 2) {
+        k[1] = fadd(a.cr, b.r, one) + T1;  // T + TR + R
+        k[2] = fadd(a.lc, a.r, one) + T2;  // TL + T + TR
+        k[3] = fadd(a.lc, b.l, one) + T3;  // L + TL + T
+        k[5] = fadd(c.lc, b.l, one) + T5;  // B + BL + L
+        k[6] = fadd(c.lc, c.r, one) + T6;  // BR + B + BL
+        k[7] = fadd(c.cr, b.r, one) + T7;  // R + BR + B
+    } else {
+        k[1] = a.cr + b.r + T1;
+        k[2] = a.lc + a.r + T2;
+        k[3] = a.lc + b.l + T3;
+        k[5] = c.lc + b.l + T5;
+        k[6] = c.lc + c.r + T6;
+        k[7] = c.cr + b.r + T7;
+    }
     return topk_id<K>(k);
 }
 
@@ -191,8 +210,17 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
         const int band = rem / p.blocks, blk = rem - band * p.blocks;
         const int r0 = band * p.band_rows;
         const int seg_rows = seg_live ? min(p.rows, r0 + p.band_rows) - r0 : 0;
-        int n_rows = seg_rows;
-        if (NSEG > 1) n_rows = max(n_rows, __shfl_xor_sync(FULL, n_rows, 16));
+        // warp-wide row count from warp-uniform quantities only (no shuffle),
+        // so the row loop's trip count is known uniform
+        int n_rows = 0;
+#pragma unroll
+        for (int sg = 0; sg < NSEG; ++sg) {
+            const int64_t tt = NSEG * wt + sg;
+            if (tt < p.n_tiles) {
+                const int bnd = int((tt % tiles_per_image) / p.blocks);
+                n_rows = max(n_rows, min(p.rows, bnd * p.band_rows + p.band_rows) - bnd * p.band_rows);
+            }
+        }
         const int c0 = blk * kTileCols;
         const int y = c0 + sl * LC;
         const uint8_t* img_px = p.px + int64_t(img) * p.img_stride;
@@ -350,19 +378,21 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
         RowN<NW> rb = unpack(load_raw(r0));
         RowN<NW> rc = unpack(load_raw(r0 + 1));
         RawN<NW> q0 = load_raw(r0 + 2), q1 = load_raw(r0 + 3), q2 = load_raw(r0 + 4);
-        for (int i = 0; i < n_rows; i += 3) {
+        int i = 0;
+        for (; i + 3 <= n_rows; i += 3) {
             step(ra, rb, rc, i);
-            if (i + 1 >= n_rows) break;
             ra = unpack(q0);
             q0 = load_raw(r0 + i + 5);
             step(rb, rc, ra, i + 1);
-            if (i + 2 >= n_rows) break;
             rb = unpack(q1);
             q1 = load_raw(r0 + i + 6);
             step(rc, ra, rb, i + 2);
-            if (i + 3 >= n_rows) break;
             rc = unpack(q2);
             q2 = load_raw(r0 + i + 7);
+        }
+        if (i < n_rows) {  // 1 or 2 remaining rows
+            step(ra, rb, rc, i);
+            if (i + 1 < n_rows) step(rb, rc, unpack(q0), i + 1);
         }
 
         // ---- cell border columns: recount with the cell clamp ----
