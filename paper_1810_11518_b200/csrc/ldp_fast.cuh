@@ -29,6 +29,11 @@
 // loop with the outside row replaced by the row itself; border columns are
 // masked out of the main count and recounted afterwards from clamped loads.
 #pragma once
+#include <type_traits>
+
+#ifndef ALDP_SIMPLE
+#define ALDP_SIMPLE 1
+#endif
 
 namespace aldp_b200 {
 
@@ -193,6 +198,23 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
     __syncthreads();
 
     const int64_t tiles_per_image = int64_t(p.bands) * p.blocks;
+    // Tile order: groups of G images (G = 2 when an image row has an odd
+    // number of 128-column blocks), band-major inside a group, so the two
+    // tiles a warp runs together always share a band (same height) -- the
+    // warp then takes the predicate-free path. Neighbouring bands of an image
+    // stay close in time, so band halos hit L2.
+    const int G = (p.blocks & 1) ? 2 : 1;
+    auto tile_coords = [&](int64_t tt, int& img_, int& band_, int& blk_) {
+        const int64_t grp = tt / (G * tiles_per_image);
+        const int64_t t_in = tt - grp * G * tiles_per_image;
+        const int64_t left_ = p.n_images - grp * G;
+        const int gi = left_ < G ? int(left_) : G;  // images in this group
+        const int per_band = gi * p.blocks;
+        band_ = int(t_in / per_band);
+        const int rem_ = int(t_in - int64_t(band_) * per_band);
+        img_ = int(grp * G) + rem_ / p.blocks;
+        blk_ = rem_ % p.blocks;
+    };
     const int64_t warp_global = int64_t(blockIdx.x) * kFastWarps + warp;
     const int64_t warp_stride = int64_t(gridDim.x) * kFastWarps;
     const uint32_t seg_lane0 = uint32_t(seg * SEG);
@@ -205,9 +227,8 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
         const int64_t tile = NSEG * wt + seg;
         const bool seg_live = tile < p.n_tiles;
         const int64_t t = seg_live ? tile : p.n_tiles - 1;
-        const int img = int(t / tiles_per_image);
-        const int rem = int(t - int64_t(img) * tiles_per_image);
-        const int band = rem / p.blocks, blk = rem - band * p.blocks;
+        int img, band, blk;
+        tile_coords(t, img, band, blk);
         const int r0 = band * p.band_rows;
         const int seg_rows = seg_live ? min(p.rows, r0 + p.band_rows) - r0 : 0;
         // warp-wide row count from warp-uniform quantities only (no shuffle),
@@ -217,7 +238,8 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
         for (int sg = 0; sg < NSEG; ++sg) {
             const int64_t tt = NSEG * wt + sg;
             if (tt < p.n_tiles) {
-                const int bnd = int((tt % tiles_per_image) / p.blocks);
+                int im_, bnd, bk_;
+                tile_coords(tt, im_, bnd, bk_);
                 n_rows = max(n_rows, min(p.rows, bnd * p.band_rows + p.band_rows) - bnd * p.band_rows);
             }
         }
@@ -259,15 +281,19 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
             }
         }
 
+        // per-lane row-0 pointers; a row load adds one IMAD.WIDE per pointer
+        const uint8_t* const own_p = img_px + own_off;
+        const uint8_t* const halo_p = img_px + halo_off;
+        const uint8_t* const pf_p = img_px + c0;
         auto load_raw = [&](int r) -> RawN<NW> {
-            const uint8_t* rowp = img_px + int64_t(min(max(r, 0), p.rows - 1)) * p.pitch;
+            const int rr = min(max(r, 0), p.rows - 1);
             if (sl == 1) {  // pull a row further ahead into L2
-                const uint8_t* ahead = img_px + int64_t(min(max(r + kL2Ahead, 0), p.rows - 1)) * p.pitch + c0;
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(ahead));
+                const int ra_ = min(r + kL2Ahead, p.rows - 1);
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(pf_p + (long long)ra_ * p.pitch));
             }
             RawN<NW> q;
-            load_words<NW>(rowp + own_off, q.w);
-            q.h = halo_lane ? __ldg(reinterpret_cast<const uint32_t*>(rowp + halo_off)) : 0u;
+            load_words<NW>(own_p + (long long)rr * p.pitch, q.w);
+            q.h = halo_lane ? __ldg(reinterpret_cast<const uint32_t*>(halo_p + (long long)rr * p.pitch)) : 0u;
             return q;
         };
         auto unpack = [&](const RawN<NW>& q) -> RowN<NW> {
@@ -316,8 +342,13 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
             }
             slot[s] = on ? seg_base + uint32_t(lc) * kRegion + 256 : trash;
         }
-        uint8_t* dst = CODES ? p.codes + int64_t(img) * p.codes_img_stride : nullptr;
+        // per-lane code-map pointer at row r0; a row's store adds one IMAD.WIDE
+        uint8_t* const lane_dst =
+            CODES ? p.codes + int64_t(img) * p.codes_img_stride + int64_t(r0) * p.codes_pitch + y : nullptr;
         const bool lane_out = seg_live && y < p.cols;
+        // Common case: every lane of the warp is inside the image and on a
+        // live row of equal-height tiles -> no per-lane predication at all.
+        const bool simple = __all_sync(FULL, lane_out && seg_rows == n_rows);
 
         // Slot addresses of the lane's pixel ids. Pair q = 2j (P_A of word
         // j) covers columns y+4j (lo) / y+4j+2 (hi); q = 2j+1 (P_B) covers
@@ -338,11 +369,14 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
             }
         };
 
-        auto step = [&](const RowN<NW>& a, const RowN<NW>& b, const RowN<NW>& c, int i) {
+        // SIMPLE (a std::integral_constant) drops the per-lane live/in-image
+        // predicates for warps that need none.
+        auto step = [&](auto simple_tag, const RowN<NW>& a, const RowN<NW>& b, const RowN<NW>& c, int i) {
+            constexpr bool SIMPLE = decltype(simple_tag)::value;
             uint32_t X[NPAIR], ad[LC];
             row_ids(a, b, c, X);
             addrs(X, ad);
-            const bool live = i < seg_rows;
+            const bool live = SIMPLE || i < seg_rows;
             if (CODES) {
                 uint32_t e[LC];
 #pragma unroll
@@ -351,8 +385,8 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
 #pragma unroll
                 for (int j = 0; j < NW; ++j)  // bytes -> word with multiply-adds (FMA pipe)
                     wd[j] = e[4 * j] + e[4 * j + 1] * 0x100u + e[4 * j + 2] * 0x10000u + e[4 * j + 3] * 0x1000000u;
-                if (live && lane_out) {
-                    uint8_t* o = dst + int64_t(r0 + i) * p.codes_pitch + y;
+                if (SIMPLE || (live && lane_out)) {
+                    uint8_t* o = lane_dst + (long long)i * p.codes_pitch;
                     if constexpr (NW == 1) *reinterpret_cast<uint32_t*>(o) = wd[0];
                     else *reinterpret_cast<uint2*>(o) = make_uint2(wd[0], wd[1]);
                 }
@@ -374,26 +408,30 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
         };
 
         // ---- main loop: rows r0 .. r0+n_rows-1, unrolled by 3 ----
-        RowN<NW> ra = unpack(load_raw(r0 - 1));
-        RowN<NW> rb = unpack(load_raw(r0));
-        RowN<NW> rc = unpack(load_raw(r0 + 1));
-        RawN<NW> q0 = load_raw(r0 + 2), q1 = load_raw(r0 + 3), q2 = load_raw(r0 + 4);
-        int i = 0;
-        for (; i + 3 <= n_rows; i += 3) {
-            step(ra, rb, rc, i);
-            ra = unpack(q0);
-            q0 = load_raw(r0 + i + 5);
-            step(rb, rc, ra, i + 1);
-            rb = unpack(q1);
-            q1 = load_raw(r0 + i + 6);
-            step(rc, ra, rb, i + 2);
-            rc = unpack(q2);
-            q2 = load_raw(r0 + i + 7);
-        }
-        if (i < n_rows) {  // 1 or 2 remaining rows
-            step(ra, rb, rc, i);
-            if (i + 1 < n_rows) step(rb, rc, unpack(q0), i + 1);
-        }
+        auto run_rows = [&](auto simple_tag) {
+            RowN<NW> ra = unpack(load_raw(r0 - 1));
+            RowN<NW> rb = unpack(load_raw(r0));
+            RowN<NW> rc = unpack(load_raw(r0 + 1));
+            RawN<NW> q0 = load_raw(r0 + 2), q1 = load_raw(r0 + 3), q2 = load_raw(r0 + 4);
+            int i = 0;
+            for (; i + 3 <= n_rows; i += 3) {
+                step(simple_tag, ra, rb, rc, i);
+                ra = unpack(q0);
+                q0 = load_raw(r0 + i + 5);
+                step(simple_tag, rb, rc, ra, i + 1);
+                rb = unpack(q1);
+                q1 = load_raw(r0 + i + 6);
+                step(simple_tag, rc, ra, rb, i + 2);
+                rc = unpack(q2);
+                q2 = load_raw(r0 + i + 7);
+            }
+            if (i < n_rows) {  // 1 or 2 remaining rows
+                step(simple_tag, ra, rb, rc, i);
+                if (i + 1 < n_rows) step(simple_tag, rb, rc, unpack(q0), i + 1);
+            }
+        };
+        if (ALDP_SIMPLE && simple) run_rows(std::integral_constant<bool, true>{});
+        else run_rows(std::integral_constant<bool, false>{});
 
         // ---- cell border columns: recount with the cell clamp ----
         if (HIST && CELLS && __any_sync(FULL, do_hist)) {

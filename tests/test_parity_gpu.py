@@ -263,3 +263,18 @@ def test_empty_batch_and_constant_images():
     torch.cuda.synchronize()
     assert bool((c[:, :, :16] == 7).all())            # total tie -> code 7 (bin 0)
     assert int(h[0, 0, 0]) == 160 and int(h.sum()) == 320
+
+
+@pytest.mark.parametrize("n,rows,cols,cell", [(3, 490, 640, (81, 91)), (5, 130, 384, (0, 0)),
+                                              (1, 97, 640, (32, 40)), (7, 64, 128, (16, 16))])
+def test_odd_image_counts_and_block_parity(n, rows, cols, cell):
+    """Tile pairing groups two images when a row has an odd number of
+    128-column blocks; odd image counts leave a partial group."""
+    px = aldp.gen_faces(n, rows, cols, blobs=10, seed=n * 31 + cols, device=DEV)
+    torch.cuda.synchronize()
+    host = px[:, :, :cols].cpu().numpy()
+    want_c, want_h = oracle.batch(host, k=3, cell=cell)
+    for kern in ("fast", "generic"):
+        c, h = run(host, 3, cell=cell, kernel=kern)
+        assert np.array_equal(c, want_c), kern
+        assert np.array_equal(h, want_h), kern
