@@ -35,11 +35,12 @@
 #define ALDP_SIMPLE 1
 #endif
 
+
 namespace aldp_b200 {
 
 constexpr int kFastWarps = 8;
 constexpr int kTileCols = 128;
-constexpr int kMaxTileCells = 3;
+constexpr int kMaxTileCells = 5;
 constexpr uint32_t kScaleMask = 0x3FC03FC0u;  // bytes 0 and 2 of a word, scaled by 64
 // Per-segment shared layout: kMaxTileCells regions + 1 trash region; a region
 // is [id->code table copy (256 B) | counts (256 B)].
@@ -130,16 +131,20 @@ __device__ __forceinline__ uint32_t pair_id(const Col& a, const Col& b, const Co
 template <int NW>
 struct RowN {
     uint32_t A[NW], B[NW], L[NW], R[NW];
-    uint32_t la[NW], ab[NW], br[NW];
+    uint32_t la[NW], ab[NW], br[NW];  // filled only when the kernel keeps row sums
 };
 
-template <int NW>
+// SUMS: take the row's stored pair sums, else add on use (fewer live
+// registers for the register-tight cell-mode kernel, a few more adds).
+template <bool SUMS, int NW>
 __device__ __forceinline__ Col colA(const RowN<NW>& r, int j) {  // pair P_A of word j
-    return Col{r.L[j], r.A[j], r.B[j], r.la[j], r.ab[j]};
+    if constexpr (SUMS) return Col{r.L[j], r.A[j], r.B[j], r.la[j], r.ab[j]};
+    else return Col{r.L[j], r.A[j], r.B[j], r.L[j] + r.A[j], r.A[j] + r.B[j]};
 }
-template <int NW>
+template <bool SUMS, int NW>
 __device__ __forceinline__ Col colB(const RowN<NW>& r, int j) {  // pair P_B of word j
-    return Col{r.A[j], r.B[j], r.R[j], r.ab[j], r.br[j]};
+    if constexpr (SUMS) return Col{r.A[j], r.B[j], r.R[j], r.ab[j], r.br[j]};
+    else return Col{r.A[j], r.B[j], r.R[j], r.A[j] + r.B[j], r.B[j] + r.R[j]};
 }
 
 template <int NW>
@@ -175,6 +180,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
     constexpr int NSEG = 32 / SEG;          // tiles per warp
     constexpr int NPAIR = 2 * NW;           // u16x2 pixel pairs per lane
     constexpr unsigned FULL = 0xffffffffu;
+    constexpr bool SUMS = !CELLS;           // measured: stored sums win only without cells
     extern __shared__ __align__(512) uint8_t smem[];
     __shared__ uint8_t id_bin[64];
     __shared__ int fix_cols[kFastWarps][NSEG][kFixList];
@@ -320,9 +326,11 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
             for (int j = 0; j < NW; ++j) {
                 r.L[j] = prmt(r.B[j], j == 0 ? prevB : r.B[j - 1], 0x1076);       // (y+4j-1, y+4j+1)
                 r.R[j] = prmt(r.A[j], j == NW - 1 ? nextA : r.A[j + 1], 0x5432);  // (y+4j+2, y+4j+4)
-                r.la[j] = fadd(r.L[j], r.A[j], one);
-                r.ab[j] = fadd(r.A[j], r.B[j], one);
-                r.br[j] = fadd(r.B[j], r.R[j], one);
+                if constexpr (SUMS) {
+                    r.la[j] = fadd(r.L[j], r.A[j], one);
+                    r.ab[j] = fadd(r.A[j], r.B[j], one);
+                    r.br[j] = fadd(r.B[j], r.R[j], one);
+                }
             }
             return r;
         };
@@ -364,8 +372,8 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
         auto row_ids = [&](const RowN<NW>& a, const RowN<NW>& b, const RowN<NW>& c, uint32_t (&X)[NPAIR]) {
 #pragma unroll
             for (int j = 0; j < NW; ++j) {
-                X[2 * j] = pair_id<K>(colA(a, j), colA(b, j), colA(c, j), one);
-                X[2 * j + 1] = pair_id<K>(colB(a, j), colB(b, j), colB(c, j), one);
+                X[2 * j] = pair_id<K>(colA<SUMS>(a, j), colA<SUMS>(b, j), colA<SUMS>(c, j), one);
+                X[2 * j + 1] = pair_id<K>(colB<SUMS>(a, j), colB<SUMS>(b, j), colB<SUMS>(c, j), one);
             }
         };
 

@@ -247,7 +247,7 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
     const bool fast_ok = aligned && a->k != 4 && ncl <= kMaxTileCells;
     if (kernel == ALDP_KERNEL_FAST && !fast_ok)
         return fail(ALDP_EINVAL, "fast kernel needs cols % 4 == 0, aligned pitches/strides, "
-                                 "k != 4 and at most 3 cells per 128 columns");
+                                 "k != 4 and at most 5 cells per 128 columns");
     if (kernel != ALDP_KERNEL_GENERIC && fast_ok) {
         FastParams p{};
         p.px = a->d_pixels;
