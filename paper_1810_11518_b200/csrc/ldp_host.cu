@@ -33,9 +33,14 @@ static aldp_status hfail(aldp_status s, const std::string& msg) { return set_err
                          std::string(#expr) + ": " + cudaGetErrorString(_e));               \
     } while (0)
 
-// Per host thread: a stream and grow-only device buffers.
-struct HostCtx {
-    int device = -1;
+// Per host thread: kSlots streams, each with grow-only device buffers for one
+// chunk of images. A batch is cut into chunks that rotate over the slots, so
+// chunk i+1's H2D, chunk i's kernel and chunk i-1's D2H run concurrently
+// (separate copy engines per direction; stream order protects buffer reuse).
+constexpr int kSlots = 3;
+constexpr size_t kChunkBytes = size_t(48) << 20;  // pixel bytes per chunk (~150 640x490 frames)
+
+struct Slot {
     cudaStream_t stream = nullptr;
     uint8_t* d_px = nullptr;
     size_t px_cap = 0;
@@ -43,15 +48,21 @@ struct HostCtx {
     size_t codes_cap = 0;
     uint32_t* d_hist = nullptr;
     size_t hist_cap = 0;
-    uint32_t* h_hist = nullptr;  // pinned staging for u32 -> u64 widening
-    size_t h_hist_cap = 0;
-    ~HostCtx() {
-        // Process teardown: the CUDA context may already be gone; ignore errors.
+    void release() {
         if (d_px) cudaFree(d_px);
         if (d_codes) cudaFree(d_codes);
         if (d_hist) cudaFree(d_hist);
-        if (h_hist) cudaFreeHost(h_hist);
         if (stream) cudaStreamDestroy(stream);
+        *this = Slot{};
+    }
+};
+
+struct HostCtx {
+    int device = -1;
+    Slot slot[kSlots];
+    ~HostCtx() {
+        // Process teardown: the CUDA context may already be gone; ignore errors.
+        for (auto& s : slot) s.release();
     }
 };
 static thread_local HostCtx t_ctx;
@@ -69,18 +80,9 @@ static aldp_status ensure(void** p, size_t* cap, size_t need) {
 static aldp_status ctx_ready(HostCtx& c) {
     int dev = 0;
     HOST_CUDA_TRY(cudaGetDevice(&dev));
-    if (c.device != dev) {
-        // a different device on this thread: drop buffers of the old one
-        if (c.d_px) cudaFree(c.d_px);
-        if (c.d_codes) cudaFree(c.d_codes);
-        if (c.d_hist) cudaFree(c.d_hist);
-        c.d_px = nullptr;
-        c.d_codes = nullptr;
-        c.d_hist = nullptr;
-        c.px_cap = c.codes_cap = c.hist_cap = 0;
-        if (c.stream) cudaStreamDestroy(c.stream);
-        c.stream = nullptr;
-        HOST_CUDA_TRY(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    if (c.device != dev) {  // a different device on this thread: drop the old buffers
+        for (auto& s : c.slot) s.release();
+        for (auto& s : c.slot) HOST_CUDA_TRY(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
         c.device = dev;
     }
     return ALDP_OK;
@@ -89,7 +91,8 @@ static aldp_status ctx_ready(HostCtx& c) {
 static int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
 // Shared body: host pixels (n contiguous rows x cols images) -> optional host
-// codes (contiguous) and device-side u32 histograms copied to `hist32`.
+// codes (contiguous) and u32 histograms `hist32` [n][cells][bins]. Pinned
+// host memory gives full PCIe rate in both directions at once.
 static aldp_status host_batch(const uint8_t* px, int n, int rows, int cols, int k, int cell_rows,
                               int cell_cols, uint8_t* codes, uint32_t* hist32, cudaStream_t user) {
     if (!px && n > 0) return hfail(ALDP_EINVAL, "null pixels");
@@ -104,55 +107,70 @@ static aldp_status host_batch(const uint8_t* px, int n, int rows, int cols, int 
     HostCtx& c = t_ctx;
     aldp_status s = ctx_ready(c);
     if (s != ALDP_OK) return s;
-    cudaStream_t st = user ? user : c.stream;
+    if (n == 0) return ALDP_OK;
     // pad the device pitch to 16 B so the packed kernel always applies
     const int pitch = round_up(cols, 16);
     const size_t img_bytes = size_t(pitch) * rows;
-    s = ensure(reinterpret_cast<void**>(&c.d_px), &c.px_cap, img_bytes * std::max(n, 1));
-    if (s != ALDP_OK) return s;
-    if (codes) {
-        s = ensure(reinterpret_cast<void**>(&c.d_codes), &c.codes_cap, img_bytes * std::max(n, 1));
-        if (s != ALDP_OK) return s;
+    const size_t plane = size_t(rows) * cols;
+    const size_t hist_per_img = size_t(cells) * nbins;
+    const int chunk = int(std::max<size_t>(1, std::min<size_t>(size_t(n), kChunkBytes / img_bytes)));
+    const int n_chunks = (n + chunk - 1) / chunk;
+    const int used = std::min(n_chunks, kSlots);
+    // order the internal streams after work already queued on the caller's stream
+    cudaEvent_t start = nullptr;
+    if (user) {
+        HOST_CUDA_TRY(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+        HOST_CUDA_TRY(cudaEventRecord(start, user));
     }
-    const size_t hist_n = size_t(n) * cells * nbins;
-    if (hist32) {
-        s = ensure(reinterpret_cast<void**>(&c.d_hist), &c.hist_cap,
-                   sizeof(uint32_t) * std::max<size_t>(hist_n, 1));
+    for (int i = 0; i < used; ++i) {
+        Slot& sl = c.slot[i];
+        s = ensure(reinterpret_cast<void**>(&sl.d_px), &sl.px_cap, img_bytes * chunk);
+        if (s == ALDP_OK && codes) s = ensure(reinterpret_cast<void**>(&sl.d_codes), &sl.codes_cap, img_bytes * chunk);
+        if (s == ALDP_OK && hist32)
+            s = ensure(reinterpret_cast<void**>(&sl.d_hist), &sl.hist_cap, sizeof(uint32_t) * hist_per_img * chunk);
         if (s != ALDP_OK) return s;
+        if (start) HOST_CUDA_TRY(cudaStreamWaitEvent(sl.stream, start, 0));
     }
-    if (n == 0) return ALDP_OK;
-    if (pitch == cols)
-        HOST_CUDA_TRY(cudaMemcpyAsync(c.d_px, px, img_bytes * n, cudaMemcpyHostToDevice, st));
-    else
-        HOST_CUDA_TRY(cudaMemcpy2DAsync(c.d_px, pitch, px, cols, cols, size_t(rows) * n,
-                                        cudaMemcpyHostToDevice, st));
-    aldp_ldp_args a{};
-    a.d_pixels = c.d_px;
-    a.img_stride = int64_t(img_bytes);
-    a.rows = rows;
-    a.cols = cols;
-    a.pitch = pitch;
-    a.n_images = n;
-    a.k = k;
-    a.cell_rows = cell_rows;
-    a.cell_cols = cell_cols;
-    a.d_codes = codes ? c.d_codes : nullptr;
-    a.codes_img_stride = int64_t(img_bytes);
-    a.codes_pitch = pitch;
-    a.d_hist = hist32 ? c.d_hist : nullptr;
-    s = aldp_ldp_batch(&a, st);
-    if (s != ALDP_OK) return hfail(s, aldp_last_error());
-    if (codes) {
+    if (start) cudaEventDestroy(start);
+    for (int ch = 0; ch < n_chunks; ++ch) {
+        Slot& sl = c.slot[ch % kSlots];
+        const cudaStream_t st = sl.stream;
+        const int i0 = ch * chunk, cnt = std::min(chunk, n - i0);
+        const uint8_t* src = px + size_t(i0) * plane;
         if (pitch == cols)
-            HOST_CUDA_TRY(cudaMemcpyAsync(codes, c.d_codes, img_bytes * n, cudaMemcpyDeviceToHost, st));
+            HOST_CUDA_TRY(cudaMemcpyAsync(sl.d_px, src, img_bytes * cnt, cudaMemcpyHostToDevice, st));
         else
-            HOST_CUDA_TRY(cudaMemcpy2DAsync(codes, cols, c.d_codes, pitch, cols, size_t(rows) * n,
-                                            cudaMemcpyDeviceToHost, st));
+            HOST_CUDA_TRY(cudaMemcpy2DAsync(sl.d_px, pitch, src, cols, cols, size_t(rows) * cnt,
+                                            cudaMemcpyHostToDevice, st));
+        aldp_ldp_args a{};
+        a.d_pixels = sl.d_px;
+        a.img_stride = int64_t(img_bytes);
+        a.rows = rows;
+        a.cols = cols;
+        a.pitch = pitch;
+        a.n_images = cnt;
+        a.k = k;
+        a.cell_rows = cell_rows;
+        a.cell_cols = cell_cols;
+        a.d_codes = codes ? sl.d_codes : nullptr;
+        a.codes_img_stride = int64_t(img_bytes);
+        a.codes_pitch = pitch;
+        a.d_hist = hist32 ? sl.d_hist : nullptr;
+        s = aldp_ldp_batch(&a, st);
+        if (s != ALDP_OK) return hfail(s, aldp_last_error());
+        if (codes) {
+            uint8_t* dst = codes + size_t(i0) * plane;
+            if (pitch == cols)
+                HOST_CUDA_TRY(cudaMemcpyAsync(dst, sl.d_codes, img_bytes * cnt, cudaMemcpyDeviceToHost, st));
+            else
+                HOST_CUDA_TRY(cudaMemcpy2DAsync(dst, cols, sl.d_codes, pitch, cols, size_t(rows) * cnt,
+                                                cudaMemcpyDeviceToHost, st));
+        }
+        if (hist32)
+            HOST_CUDA_TRY(cudaMemcpyAsync(hist32 + size_t(i0) * hist_per_img, sl.d_hist,
+                                          sizeof(uint32_t) * hist_per_img * cnt, cudaMemcpyDeviceToHost, st));
     }
-    if (hist32)
-        HOST_CUDA_TRY(cudaMemcpyAsync(hist32, c.d_hist, sizeof(uint32_t) * hist_n,
-                                      cudaMemcpyDeviceToHost, st));
-    HOST_CUDA_TRY(cudaStreamSynchronize(st));
+    for (int i = 0; i < used; ++i) HOST_CUDA_TRY(cudaStreamSynchronize(c.slot[i].stream));
     return ALDP_OK;
 }
 

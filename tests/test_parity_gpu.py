@@ -278,3 +278,22 @@ def test_odd_image_counts_and_block_parity(n, rows, cols, cell):
         c, h = run(host, 3, cell=cell, kernel=kern)
         assert np.array_equal(c, want_c), kern
         assert np.array_equal(h, want_h), kern
+
+
+def test_host_batch_pipelined_chunks():
+    """aldp_ldp_batch_host cuts large batches into chunks over 3 streams;
+    results must equal the device-resident path image for image."""
+    n = 400  # > 2 chunks of 640x490
+    px = aldp.gen_faces(n, 490, 640, blobs=20, seed=77, device=DEV)
+    codes, hist = aldp.ldp_batch(px, 490, 640, k=3, cell=(81, 91), codes=True, hist=True)
+    torch.cuda.synchronize()
+    host = px.cpu().numpy()
+    hc, hh = aldp.ldp_batch_host(host, k=3, cell=(81, 91))
+    assert np.array_equal(hc, codes.cpu().numpy())
+    assert np.array_equal(hh, hist.cpu().numpy().astype(np.uint32))
+    pinned = torch.from_numpy(host).pin_memory()
+    c2 = torch.empty_like(pinned).pin_memory()
+    h2 = torch.empty((n, 42, 56), dtype=torch.int32).pin_memory()
+    aldp._check(aldp.lib.aldp_ldp_batch_host(pinned.data_ptr(), n, 490, 640, 3, 81, 91, c2.data_ptr(),
+                                             h2.data_ptr(), None))
+    assert torch.equal(c2, codes.cpu()) and torch.equal(h2, hist.cpu())
