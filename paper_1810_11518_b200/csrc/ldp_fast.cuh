@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
         const uint8_t* const pf_p = img_px + c0;
         auto load_raw = [&](int r) -> RawN<NW> {
             const int rr = min(max(r, 0), p.rows - 1);
-            if (sl == 1) {  // pull a row further ahead into L2
+            if (!CELLS && sl == 1) {  // pull a row further ahead into L2 (measured: pays only without cells)
                 const int ra_ = min(r + kL2Ahead, p.rows - 1);
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(pf_p + (long long)ra_ * p.pitch));
             }
