@@ -87,6 +87,19 @@ __device__ __forceinline__ uint32_t vmin3(uint32_t a, uint32_t b, uint32_t c) {
     return vmin(vmin(a, b), c);
 }
 
+// max/min(a + b, c) on u16x2 lanes as one VIADDMNMX.U16x2 (b may be an
+// immediate): fuses a key's last add into its first comparator.
+__device__ __forceinline__ uint32_t vaddmax(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm("{.reg .b32 t; add.u16x2 t, %1, %2; max.u16x2 %0, t, %3;}" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+__device__ __forceinline__ uint32_t vaddmin(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm("{.reg .b32 t; add.u16x2 t, %1, %2; min.u16x2 %0, t, %3;}" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+
 // XOR of the low-six-bit tags of the top-k keys of K[0..7] (u16x2 lanes,
 // keys unique per lane). Returns the per-lane id in bits 0-5 / 16-21 plus
 // garbage in the other bits (callers mask).
@@ -96,19 +109,18 @@ __device__ __forceinline__ uint32_t vmin3(uint32_t a, uint32_t b, uint32_t c) {
 // p/q = max/min(K0,K1), r/s = max/min(K2,K3), x = min(p,r), y = max(q,s));
 // the top three of the union are then the half-cleaner maxima
 // {max(a1,b3), max(a2,b2), max(a3,b1)}. 18 min/max per two pixels.
+//
+// topk_from_pairs takes the network after its first comparator layer:
+// p/q = max/min(K0,K1), r/s = max/min(K2,K3) (half A), same for K4..K7.
 template <int K>
-__device__ __forceinline__ uint32_t topk_id(const uint32_t (&k)[8]) {
+__device__ __forceinline__ uint32_t topk_from_pairs(uint32_t pA, uint32_t qA, uint32_t rA, uint32_t sA,
+                                                    uint32_t pB, uint32_t qB, uint32_t rB, uint32_t sB) {
     static_assert(K >= 1 && K <= 7 && K != 4, "k == 4 uses the generic kernel");
     if constexpr (K == 1) {
-        return vmax3(vmax3(k[0], k[1], k[2]), vmax3(k[3], k[4], k[5]), vmax(k[6], k[7]));
+        return vmax(vmax3(pA, rA, pB), rB);
     } else if constexpr (K == 7) {  // complement of the single smallest key
-        return kTagAllXor * 0x10001u ^
-               vmin3(vmin3(k[0], k[1], k[2]), vmin3(k[3], k[4], k[5]), vmin(k[6], k[7]));
+        return kTagAllXor * 0x10001u ^ vmin(vmin3(qA, sA, qB), sB);
     } else {
-        const uint32_t pA = vmax(k[0], k[1]), qA = vmin(k[0], k[1]);
-        const uint32_t rA = vmax(k[2], k[3]), sA = vmin(k[2], k[3]);
-        const uint32_t pB = vmax(k[4], k[5]), qB = vmin(k[4], k[5]);
-        const uint32_t rB = vmax(k[6], k[7]), sB = vmin(k[6], k[7]);
         const uint32_t xA = vmin(pA, rA), yA = vmax(qA, sA);
         const uint32_t xB = vmin(pB, rB), yB = vmax(qB, sB);
         if constexpr (K == 3) {
@@ -131,6 +143,12 @@ __device__ __forceinline__ uint32_t topk_id(const uint32_t (&k)[8]) {
             return kTagAllXor * 0x10001u ^ e1 ^ e2 ^ e3;
         }
     }
+}
+
+template <int K>
+__device__ __forceinline__ uint32_t topk_id(const uint32_t (&k)[8]) {
+    return topk_from_pairs<K>(vmax(k[0], k[1]), vmin(k[0], k[1]), vmax(k[2], k[3]), vmin(k[2], k[3]),
+                              vmax(k[4], k[5]), vmin(k[4], k[5]), vmax(k[6], k[7]), vmin(k[6], k[7]));
 }
 
 // Scalar ring -> code for arbitrary k (1..7), the reference's rule stated as

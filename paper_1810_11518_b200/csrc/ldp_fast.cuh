@@ -95,36 +95,30 @@ __device__ __forceinline__ uint32_t pair_id(const Col& a, const Col& b, const Co
     constexpr uint32_t T0 = kTag(0) * 0x10001u, T1 = kTag(1) * 0x10001u, T2 = kTag(2) * 0x10001u,
                        T3 = kTag(3) * 0x10001u, T4 = kTag(4) * 0x10001u, T5 = kTag(5) * 0x10001u,
                        T6 = kTag(6) * 0x10001u, T7 = kTag(7) * 0x10001u;
-    uint32_t k[8];
-    // Pipe balance: the 3-input keys k0/k4 go to the FMA pipe (IMAD + VIADD),
-    // the 2-input keys to the ALU as one IADD3 each (ALDP_KEYMODE: 0 all
-    // IADD3, 1 this hybrid, 2 all FMA).
+    // Odd keys are never materialised: their tag add is fused into the
+    // first comparator layer (VIADDMNMX.U16x2 with an immediate), their
+    // two-term sum runs on the FMA pipe. Even keys: k0/k4 (three terms) on
+    // the FMA pipe, k2/k6 as one IADD3 (ALDP_KEYMODE 2: FMA too).
 #ifndef ALDP_KEYMODE
 #define ALDP_KEYMODE 1
 #endif
-    if constexpr (ALDP_KEYMODE == 0) {
-        k[0] = a.r + b.r + c.r + T0;
-        k[4] = a.l + b.l + c.l + T4;
-    } else {
-        k[0] = fadd(fadd(a.r, b.r, one), c.r, one) + T0;  // TR + R + BR
-        k[4] = fadd(fadd(a.l, b.l, one), c.l, one) + T4;  // BL + L + TL
-    }
+    const uint32_t k0 = fadd(fadd(a.r, b.r, one), c.r, one) + T0;  // TR + R + BR
+    const uint32_t k4 = fadd(fadd(a.l, b.l, one), c.l, one) + T4;  // BL + L + TL
+    uint32_t k2, k6;
     if constexpr (ALDP_KEYMODE == 2) {
-        k[1] = fadd(a.cr, b.r, one) + T1;  // T + TR + R
-        k[2] = fadd(a.lc, a.r, one) + T2;  // TL + T + TR
-        k[3] = fadd(a.lc, b.l, one) + T3;  // L + TL + T
-        k[5] = fadd(c.lc, b.l, one) + T5;  // B + BL + L
-        k[6] = fadd(c.lc, c.r, one) + T6;  // BR + B + BL
-        k[7] = fadd(c.cr, b.r, one) + T7;  // R + BR + B
+        k2 = fadd(a.lc, a.r, one) + T2;  // TL + T + TR
+        k6 = fadd(c.lc, c.r, one) + T6;  // BR + B + BL
     } else {
-        k[1] = a.cr + b.r + T1;
-        k[2] = a.lc + a.r + T2;
-        k[3] = a.lc + b.l + T3;
-        k[5] = c.lc + b.l + T5;
-        k[6] = c.lc + c.r + T6;
-        k[7] = c.cr + b.r + T7;
+        k2 = a.lc + a.r + T2;
+        k6 = c.lc + c.r + T6;
     }
-    return topk_id<K>(k);
+    const uint32_t s1 = fadd(a.cr, b.r, one);  // T + TR + R    (k1 - T1)
+    const uint32_t s3 = fadd(a.lc, b.l, one);  // L + TL + T    (k3 - T3)
+    const uint32_t s5 = fadd(c.lc, b.l, one);  // B + BL + L    (k5 - T5)
+    const uint32_t s7 = fadd(c.cr, b.r, one);  // R + BR + B    (k7 - T7)
+    return topk_from_pairs<K>(vaddmax(s1, T1, k0), vaddmin(s1, T1, k0), vaddmax(s3, T3, k2),
+                              vaddmin(s3, T3, k2), vaddmax(s5, T5, k4), vaddmin(s5, T5, k4),
+                              vaddmax(s7, T7, k6), vaddmin(s7, T7, k6));
 }
 
 // One unpacked row of a lane: per word j, A/B/L/R and the three pair sums.
