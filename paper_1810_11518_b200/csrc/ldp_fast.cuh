@@ -95,13 +95,25 @@ __device__ __forceinline__ uint32_t pair_id(const Col& a, const Col& b, const Co
     constexpr uint32_t T0 = kTag(0) * 0x10001u, T1 = kTag(1) * 0x10001u, T2 = kTag(2) * 0x10001u,
                        T3 = kTag(3) * 0x10001u, T4 = kTag(4) * 0x10001u, T5 = kTag(5) * 0x10001u,
                        T6 = kTag(6) * 0x10001u, T7 = kTag(7) * 0x10001u;
-    // Odd keys are never materialised: their tag add is fused into the
-    // first comparator layer (VIADDMNMX.U16x2 with an immediate), their
-    // two-term sum runs on the FMA pipe. Even keys: k0/k4 (three terms) on
-    // the FMA pipe, k2/k6 as one IADD3 (ALDP_KEYMODE 2: FMA too).
+    // Key/first-layer schemes (A/B measured on C5/C4/C3, tools/gpu_ab.sh):
+    //  3 (default): odd keys by one IADD3 each, even keys' last add fused
+    //     into the first comparator layer (VIADDMNMX.U16x2): 16 instr/pair;
+    //  1/2: odd keys fused with their tag as immediate, sums on the FMA
+    //     pipe (IMAD), even keys materialised: 20 instr/pair, fewer on ALU.
 #ifndef ALDP_KEYMODE
-#define ALDP_KEYMODE 1
+#define ALDP_KEYMODE 3
 #endif
+    if constexpr (ALDP_KEYMODE == 3) {
+        // fewest instructions: odd keys materialised by one IADD3 each, even
+        // keys fused into the comparator (one pre-add + VIADDMNMX)
+        const uint32_t k1 = a.cr + b.r + T1, k3 = a.lc + b.l + T3;
+        const uint32_t k5 = c.lc + b.l + T5, k7 = c.cr + b.r + T7;
+        const uint32_t x0 = a.r + b.r + T0, x4 = a.l + b.l + T4;   // + c.r / + c.l fused
+        const uint32_t x2 = a.lc + T2, x6 = c.lc + T6;             // + a.r / + c.r fused
+        return topk_from_pairs<K>(vaddmax(x0, c.r, k1), vaddmin(x0, c.r, k1), vaddmax(x2, a.r, k3),
+                                  vaddmin(x2, a.r, k3), vaddmax(x4, c.l, k5), vaddmin(x4, c.l, k5),
+                                  vaddmax(x6, c.r, k7), vaddmin(x6, c.r, k7));
+    } else {
     const uint32_t k0 = fadd(fadd(a.r, b.r, one), c.r, one) + T0;  // TR + R + BR
     const uint32_t k4 = fadd(fadd(a.l, b.l, one), c.l, one) + T4;  // BL + L + TL
     uint32_t k2, k6;
@@ -119,6 +131,7 @@ __device__ __forceinline__ uint32_t pair_id(const Col& a, const Col& b, const Co
     return topk_from_pairs<K>(vaddmax(s1, T1, k0), vaddmin(s1, T1, k0), vaddmax(s3, T3, k2),
                               vaddmin(s3, T3, k2), vaddmax(s5, T5, k4), vaddmin(s5, T5, k4),
                               vaddmax(s7, T7, k6), vaddmin(s7, T7, k6));
+    }
 }
 
 // One unpacked row of a lane: per word j, A/B/L/R and the three pair sums.
