@@ -104,6 +104,17 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(sm)}
 
 
+def ncu_traffic_bpp():
+    """DRAM bytes/pixel of the fast kernel from the last committed ncu --set
+    full capture (profiles/traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            d = json.load(f)
+        return float(d["dram_bytes_per_pixel"]), d.get("source", "")
+    except (OSError, KeyError, ValueError):
+        return None, None
+
+
 def measured_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -324,6 +335,7 @@ def main():
 
     # ---- roofline of the dominant kernel (one launch = this rank's shard) ----
     hbm, peak_src = measured_peaks()
+    traffic_bpp, traffic_src = ncu_traffic_bpp()
     bpp_hist = hist_bytes_per_image(rows, cols, k, cr, cc) / (rows * cols)
     alg_bytes = mine * rows * cols * (2.0 + bpp_hist)
     achieved = alg_bytes / (launch_ms * 1e-3) / 1e9
@@ -339,7 +351,11 @@ def main():
                          "inputs smaller than L2: repeated steps hit L2",
                    "kernel": args.kernel},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                     "frac": round(achieved / hbm, 4), "traffic": None,
+                     "frac": round(achieved / hbm, 4),
+                     "traffic": (round(traffic_bpp * mine * rows * cols / (launch_ms * 1e-3) / 1e9, 1)
+                                 if traffic_bpp and args.config == "c5" else None),
+                     "traffic_unit": "GB/s (ncu dram bytes per pixel x pixels per launch / launch time)",
+                     "traffic_source": traffic_src,
                      "peak_source": peak_src,
                      "bytes_per_pixel": round(2.0 + bpp_hist, 4),
                      "launch_ms": round(launch_ms, 4)},
