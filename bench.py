@@ -44,6 +44,8 @@ CONFIGS = {
     "c4": (1, 16384, 16384, 3, 64, 64, 200, "faces", 42),
     "c3": (256, 1024, 1024, 3, 0, 0, 0, "ties", 11518),
     "c1": (1, 490, 640, 3, 0, 0, 0, "random", 42),
+    # diagnostic: C5 images with whole-image histograms (cost of the cell grid)
+    "c5w": (65536, 490, 640, 3, 0, 0, 20, "faces", 11518),
 }
 WORKLOAD_NAMES = {
     "c5": "C5: 65536 x 640x490 face-like, LDP k=3, code map + 7x6 cell histograms",
@@ -51,6 +53,7 @@ WORKLOAD_NAMES = {
     "c4": "C4: 16384x16384 face-like (200 blobs), LDP k=3, code map + 64x64 cell histograms",
     "c3": "C3: 256 x 1024x1024 tie-heavy, LDP k=3, code map + whole-image histograms",
     "c1": "C1: 640x490 uniform random (make_random), LDP k=3, code map + histogram",
+    "c5w": "C5 images, whole-image histograms (diagnostic)",
 }
 
 

@@ -141,16 +141,19 @@ struct RowN {
     uint32_t la[NW], ab[NW], br[NW];  // filled only when the kernel keeps row sums
 };
 
-// SUMS: take the row's stored pair sums, else add on use (fewer live
-// registers for the register-tight cell-mode kernel, a few more adds).
-template <bool SUMS, int NW>
+// SUMS: 2 = take the row's three stored pair sums; 1 = store only ab (shared
+// by both pairs of a word) and add la/br on use; 0 = add all on use (fewest
+// live registers for the register-tight cell-mode kernel, a few more adds).
+template <int SUMS, int NW>
 __device__ __forceinline__ Col colA(const RowN<NW>& r, int j) {  // pair P_A of word j
-    if constexpr (SUMS) return Col{r.L[j], r.A[j], r.B[j], r.la[j], r.ab[j]};
+    if constexpr (SUMS == 2) return Col{r.L[j], r.A[j], r.B[j], r.la[j], r.ab[j]};
+    else if constexpr (SUMS == 1) return Col{r.L[j], r.A[j], r.B[j], r.L[j] + r.A[j], r.ab[j]};
     else return Col{r.L[j], r.A[j], r.B[j], r.L[j] + r.A[j], r.A[j] + r.B[j]};
 }
-template <bool SUMS, int NW>
+template <int SUMS, int NW>
 __device__ __forceinline__ Col colB(const RowN<NW>& r, int j) {  // pair P_B of word j
-    if constexpr (SUMS) return Col{r.A[j], r.B[j], r.R[j], r.ab[j], r.br[j]};
+    if constexpr (SUMS == 2) return Col{r.A[j], r.B[j], r.R[j], r.ab[j], r.br[j]};
+    else if constexpr (SUMS == 1) return Col{r.A[j], r.B[j], r.R[j], r.ab[j], r.B[j] + r.R[j]};
     else return Col{r.A[j], r.B[j], r.R[j], r.A[j] + r.B[j], r.B[j] + r.R[j]};
 }
 
@@ -187,7 +190,10 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
     constexpr int NSEG = 32 / SEG;          // tiles per warp
     constexpr int NPAIR = 2 * NW;           // u16x2 pixel pairs per lane
     constexpr unsigned FULL = 0xffffffffu;
-    constexpr bool SUMS = !CELLS;           // measured: stored sums win only without cells
+#ifndef ALDP_CELL_SUMS
+#define ALDP_CELL_SUMS 0
+#endif
+    constexpr int SUMS = CELLS ? ALDP_CELL_SUMS : 2;  // measured: all stored sums win only without cells
     extern __shared__ __align__(512) uint8_t smem[];
     __shared__ uint8_t id_bin[64];
     __shared__ int fix_cols[kFastWarps][NSEG][kFixList];
@@ -333,9 +339,9 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
             for (int j = 0; j < NW; ++j) {
                 r.L[j] = prmt(r.B[j], j == 0 ? prevB : r.B[j - 1], 0x1076);       // (y+4j-1, y+4j+1)
                 r.R[j] = prmt(r.A[j], j == NW - 1 ? nextA : r.A[j + 1], 0x5432);  // (y+4j+2, y+4j+4)
-                if constexpr (SUMS) {
+                if constexpr (SUMS >= 1) r.ab[j] = fadd(r.A[j], r.B[j], one);
+                if constexpr (SUMS == 2) {
                     r.la[j] = fadd(r.L[j], r.A[j], one);
-                    r.ab[j] = fadd(r.A[j], r.B[j], one);
                     r.br[j] = fadd(r.B[j], r.R[j], one);
                 }
             }
