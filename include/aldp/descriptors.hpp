@@ -37,6 +37,20 @@ struct LdpHistogram {
 /// Runs on the B200 (both paths: outputs identical by contract).
 LdpHistogram ldp_histogram(const GrayImage& img, int k, ResponsePath path);
 
+struct LbpHistogram {
+    std::array<std::uint64_t, 256> bins{};
+    std::uint64_t total() const;
+    bool operator==(const LbpHistogram&) const = default;
+};
+
+/// Binary pattern of the 3x3 neighbourhood: ring neighbour i (clockwise
+/// from the top-left) contributes 2^i when >= the centre. Host helper.
+std::uint8_t lbp_code(const GrayImage& img, int x, int y, BorderPolicy policy = BorderPolicy::Clamp,
+                      OpCounter* counter = nullptr);
+
+/// 256-bin pattern histogram over every pixel (clamped borders), on the B200.
+LbpHistogram lbp_histogram(const GrayImage& img, BorderPolicy policy = BorderPolicy::Clamp);
+
 /// NEW: the whole-image code map, codes[x*cols+y] = ldp_code(responses(x,y), k),
 /// on the B200. Any k in [1, 7].
 std::vector<std::uint8_t> ldp_code_map(const GrayImage& img, int k = 3,

@@ -46,6 +46,8 @@ typedef enum {
  * identical outputs by contract (descriptors.hpp:53-54); both run the same
  * B200 kernel. */
 enum { ALDP_PATH_NAIVE = 0, ALDP_PATH_ACCELERATED = 1 };
+/* Descriptor selector for aldp_windowed_features: LBP (Descriptor::Lbp). */
+enum { ALDP_DESC_LBP = 2 };
 
 /* One batched launch over device-resident images.
  *
@@ -87,6 +89,13 @@ aldp_status aldp_ldp_batch(const aldp_ldp_args* args, void* stream);
 enum { ALDP_KERNEL_AUTO = 0, ALDP_KERNEL_FAST = 1, ALDP_KERNEL_GENERIC = 2 };
 aldp_status aldp_ldp_batch_ex(const aldp_ldp_args* args, int kernel, void* stream);
 
+/* LBP descriptor (descriptors.cpp:141-168): code bit i set when ring
+ * neighbour i (clockwise from the top-left) >= the centre pixel; 256 bins
+ * indexed by the code. Same argument block as aldp_ldp_batch (k ignored),
+ * d_hist is uint32 [n_images][grid_cells][256]. Same border and cell rules. */
+aldp_status aldp_lbp_batch(const aldp_ldp_args* args, void* stream);
+aldp_status aldp_lbp_batch_ex(const aldp_ldp_args* args, int kernel, void* stream);
+
 /* Number of histogram bins for k: C(8, k) (56 for k == 3), 0 if k invalid. */
 int aldp_n_bins(int k);
 
@@ -104,10 +113,11 @@ int64_t aldp_grid_cells(int rows, int cols, int cell_rows, int cell_cols);
 aldp_status aldp_ldp_histogram(const uint8_t* pixels, int rows, int cols, int k, int path,
                                uint64_t* bins56);
 
-/* aldp::windowed_features for Descriptor::Ldp / ::Aldp
- * (include/aldp/windowing.hpp:34-36): out is [grid_cells][56] uint64 in
- * row-major window order; out_len must be >= cells*56. window < 3 or larger
- * than the image -> ALDP_EINVAL (windowing.cpp:9-17). */
+/* aldp::windowed_features (include/aldp/windowing.hpp:34-36): path selects
+ * Descriptor::Ldp / ::Aldp (ALDP_PATH_NAIVE / _ACCELERATED, 56 bins per
+ * window) or ::Lbp (ALDP_DESC_LBP, 256 bins). out is [grid_cells][bins]
+ * uint64 in row-major window order; out_len must be >= cells*bins. window < 3
+ * or larger than the image -> ALDP_EINVAL (windowing.cpp:9-17). */
 aldp_status aldp_windowed_features(const uint8_t* pixels, int rows, int cols, int window,
                                    int path, uint64_t* out, size_t out_len);
 
@@ -115,6 +125,16 @@ aldp_status aldp_windowed_features(const uint8_t* pixels, int rows, int cols, in
  * descriptors.cpp:129-136 computes per pixel): codes[rows*cols]. */
 aldp_status aldp_ldp_code_map(const uint8_t* pixels, int rows, int cols, int k, int path,
                               uint8_t* codes);
+
+/* aldp::lbp_histogram (descriptors.hpp:66-67): 256 uint64 bins. */
+aldp_status aldp_lbp_histogram(const uint8_t* pixels, int rows, int cols, uint64_t* bins256);
+
+/* LBP code map (per-pixel lbp_code, descriptors.cpp:141-157). */
+aldp_status aldp_lbp_code_map(const uint8_t* pixels, int rows, int cols, uint8_t* codes);
+
+/* Host batch, LBP descriptor (hist uint32 [n][cells][256]). */
+aldp_status aldp_lbp_batch_host(const uint8_t* pixels, int n_images, int rows, int cols, int cell_rows,
+                                int cell_cols, uint8_t* codes, uint32_t* hist, void* stream);
 
 /* Host batch: n contiguous rows x cols images in host memory (pinned or
  * pageable) -> optional host code maps and uint32 histograms, one H2D and

@@ -22,6 +22,10 @@
  *   oracle_cell_histograms  src/windowing.cpp:8-19,35-63 (floor grid, each
  *                           cell clamped as its own image, row-major cells);
  *                           rectangular cells are this repo's extension.
+ *   oracle_lbp_code         src/descriptors.cpp:141-157 (k == 0 selects LBP
+ *                           in the map/histogram/batch functions: bit i set
+ *                           when ring neighbour i >= the centre, 256 bins
+ *                           indexed by the code, descriptors.cpp:159-168)
  *
  * Parity pins: tests/test_oracle.py checks this file against the reference's
  * golden fixtures (tests/golden/, converted by tests/golden/make_golden.py)
@@ -150,6 +154,7 @@ static int popcount8(unsigned c) {
 /* descriptors.cpp:25-45,104-106: rank of `code` among the codes with the same
  * popcount k, ascending by value; -1 if popcount(code) != k. */
 int oracle_bin_index(int code, int k) {
+    if (k == 0) return (code >= 0 && code <= 255) ? code : -1;
     if (code < 0 || code > 255 || popcount8((unsigned)code) != k) return -1;
     int rank = 0;
     for (int c = 0; c < code; ++c)
@@ -157,16 +162,33 @@ int oracle_bin_index(int code, int k) {
     return rank;
 }
 
-/* C(8, k): number of bins for popcount-k codes (56 for k = 3). */
+/* C(8, k): number of bins for popcount-k codes (56 for k = 3); 256 for
+ * k == 0 (LBP). */
 int oracle_n_bins(int k) {
+    if (k == 0) return 256;
     if (k < 1 || k > 7) return -1;
     int n = 0;
     for (int c = 0; c < 256; ++c) n += popcount8((unsigned)c) == k;
     return n;
 }
 
+/* descriptors.cpp:141-157: bit i set when ring neighbour i >= the centre. */
+static int lbp_win(const uint8_t* px, int pitch, int x0, int y0, int rows, int cols, int x, int y) {
+    const int centre = sample_win(px, pitch, x0, y0, rows, cols, x, y);
+    int code = 0;
+    for (int i = 0; i < 8; ++i)
+        if (sample_win(px, pitch, x0, y0, rows, cols, x + kRing[i][0], y + kRing[i][1]) >= centre)
+            code |= 1 << i;
+    return code;
+}
+
+int oracle_lbp_code(const uint8_t* px, int rows, int cols, int x, int y) {
+    return lbp_win(px, cols, 0, 0, rows, cols, x, y);
+}
+
 static int code_win(const uint8_t* px, int pitch, int x0, int y0, int rows, int cols, int x,
                     int y, int k) {
+    if (k == 0) return lbp_win(px, pitch, x0, y0, rows, cols, x, y);
     int m[8];
     responses_win(px, pitch, x0, y0, rows, cols, x, y, m);
     return oracle_ldp_code(m, k);
@@ -175,7 +197,7 @@ static int code_win(const uint8_t* px, int pitch, int x0, int y0, int rows, int 
 /* The per-pixel code of descriptors.cpp:129-136 written out as a map:
  * codes[x * cols + y] = ldp_code(responses(img, x, y), k). Image clamp. */
 int oracle_code_map(const uint8_t* px, int rows, int cols, int k, uint8_t* codes) {
-    if (k < 1 || k > 7 || rows < 3 || cols < 3) return -1;
+    if (k < 0 || k > 7 || rows < 3 || cols < 3) return -1;
     for (int x = 0; x < rows; ++x)
         for (int y = 0; y < cols; ++y)
             codes[(size_t)x * cols + y] = (uint8_t)code_win(px, cols, 0, 0, rows, cols, x, y, k);
@@ -196,7 +218,7 @@ static void rank_table(int k, int* rank) {
 
 /* descriptors.cpp:123-139 (k == 3 there; any k in [1,7] here, C(8,k) bins). */
 int oracle_histogram(const uint8_t* px, int rows, int cols, int k, uint64_t* hist) {
-    if (k < 1 || k > 7 || rows < 3 || cols < 3) return -1;
+    if (k < 0 || k > 7 || rows < 3 || cols < 3) return -1;
     int rank[256];
     rank_table(k, rank);
     memset(hist, 0, sizeof(uint64_t) * (size_t)oracle_n_bins(k));
@@ -212,7 +234,7 @@ int oracle_histogram(const uint8_t* px, int rows, int cols, int k, uint64_t* his
  * make_grid, windowing.cpp:9-17). */
 int oracle_cell_histograms(const uint8_t* px, int rows, int cols, int cell_rows,
                            int cell_cols, int k, uint64_t* hist) {
-    if (k < 1 || k > 7 || rows < 3 || cols < 3) return -1;
+    if (k < 0 || k > 7 || rows < 3 || cols < 3) return -1;
     if (cell_rows < 3 || cell_cols < 3 || cell_rows > rows || cell_cols > cols) return -1;
     const int gr = rows / cell_rows, gc = cols / cell_cols, nb = oracle_n_bins(k);
     int rank[256];
@@ -252,7 +274,7 @@ static void* batch_worker(void* arg) {
 
 int oracle_batch(const uint8_t* px, int64_t n, int rows, int cols, int k, int cell_rows,
                  int cell_cols, uint8_t* codes, uint64_t* hist, int threads) {
-    if (k < 1 || k > 7 || rows < 3 || cols < 3 || n < 0) return -1;
+    if (k < 0 || k > 7 || rows < 3 || cols < 3 || n < 0) return -1;
     int cells = 1;
     if (cell_rows != 0) {
         if (cell_rows < 3 || cell_cols < 3 || cell_rows > rows || cell_cols > cols) return -1;

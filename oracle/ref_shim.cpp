@@ -17,6 +17,8 @@
 //   ref_windowed         aldp::windowed_features          (src/windowing.cpp:35-63)
 //   ref_cell_histograms  aldp::crop + aldp::ldp_histogram (rectangular cells,
 //                        the composition windowed_features performs per window)
+//   k == 0 selects LBP: aldp::lbp_code / aldp::lbp_histogram
+//                        (src/descriptors.cpp:141-168), windowed_features(Lbp)
 //   ref_batch            the above over a batch, std::thread sharded by image
 //                        (the reference functions are pure)
 #include <cstdint>
@@ -59,6 +61,12 @@ aldp::ResponsePath path_of(int path) {
 }
 
 void code_map(const aldp::GrayImage& img, int k, aldp::ResponsePath path, uint8_t* out) {
+    if (k == 0) {
+        for (int x = 0; x < img.rows(); ++x)
+            for (int y = 0; y < img.cols(); ++y)
+                out[static_cast<size_t>(x) * img.cols() + y] = aldp::lbp_code(img, x, y);
+        return;
+    }
     for (int x = 0; x < img.rows(); ++x)
         for (int y = 0; y < img.cols(); ++y) {
             const aldp::ResponseVector r =
@@ -73,6 +81,11 @@ void code_map(const aldp::GrayImage& img, int k, aldp::ResponsePath path, uint8_
 // (descriptors.cpp:124-126), so for k != 3 the codes are counted into C(8,k)
 // ascending bins -- the repo's documented extension.
 void histogram(const aldp::GrayImage& img, int k, aldp::ResponsePath path, uint64_t* out) {
+    if (k == 0) {
+        const aldp::LbpHistogram h = aldp::lbp_histogram(img);
+        std::memcpy(out, h.bins.data(), sizeof(uint64_t) * 256);
+        return;
+    }
     if (k == 3) {
         const aldp::LdpHistogram h = aldp::ldp_histogram(img, 3, path);
         std::memcpy(out, h.bins.data(), sizeof(uint64_t) * 56);
@@ -88,6 +101,7 @@ void histogram(const aldp::GrayImage& img, int k, aldp::ResponsePath path, uint6
 }
 
 int n_bins(int k) {
+    if (k == 0) return 256;
     int nb = 0;
     for (int c = 0; c < 256; ++c) nb += __builtin_popcount(c) == k;
     return nb;
@@ -95,11 +109,13 @@ int n_bins(int k) {
 
 void cell_histograms(const aldp::GrayImage& img, int cr, int cc, int k, aldp::ResponsePath path,
                      uint64_t* out) {
-    if (cr == cc && k == 3) {  // square windows: the reference entry point itself
-        const auto feats = aldp::windowed_features(
-            img, cr, path == aldp::ResponsePath::Naive ? aldp::Descriptor::Ldp : aldp::Descriptor::Aldp);
+    if (cr == cc && (k == 3 || k == 0)) {  // square windows: the reference entry point itself
+        const auto d = k == 0 ? aldp::Descriptor::Lbp
+                              : path == aldp::ResponsePath::Naive ? aldp::Descriptor::Ldp : aldp::Descriptor::Aldp;
+        const auto feats = aldp::windowed_features(img, cr, d);
+        const size_t nb = k == 0 ? 256 : 56;
         for (size_t w = 0; w < feats.size(); ++w)
-            std::memcpy(out + w * 56, feats[w].data(), sizeof(uint64_t) * 56);
+            std::memcpy(out + w * nb, feats[w].data(), sizeof(uint64_t) * nb);
         return;
     }
     if (cr < 3 || cc < 3 || cr > img.rows() || cc > img.cols())

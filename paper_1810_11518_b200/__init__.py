@@ -35,6 +35,7 @@ __all__ = [
     "ResponsePath", "Descriptor", "AldpError", "lib", "LIB_PATH", "n_bins", "grid_cells",
     "WindowGrid", "make_grid", "ldp_histogram", "windowed_features", "ldp_code_map",
     "ldp_batch", "ldp_batch_host", "gen_faces", "gen_ties", "version",
+    "lbp_histogram", "lbp_code_map", "lbp_batch",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -98,6 +99,11 @@ def _load() -> ctypes.CDLL:
         "aldp_windowed_features": ([P, I, I, I, I, P, ctypes.c_size_t], I),
         "aldp_ldp_code_map": ([P, I, I, I, I, P], I),
         "aldp_ldp_batch_host": ([P, I, I, I, I, I, I, P, P, P], I),
+        "aldp_lbp_batch": ([ctypes.POINTER(_Args), P], I),
+        "aldp_lbp_batch_ex": ([ctypes.POINTER(_Args), I, P], I),
+        "aldp_lbp_histogram": ([P, I, I, P], I),
+        "aldp_lbp_code_map": ([P, I, I, P], I),
+        "aldp_lbp_batch_host": ([P, I, I, I, I, I, P, P, P], I),
         "aldp_last_error": ([], ctypes.c_char_p),
         "aldp_gen_faces": ([P, I, I, I, I, I64, I, U64, I64, P], I),
         "aldp_gen_ties": ([P, I, I, I, I, I64, U64, I64, P], I),
@@ -181,19 +187,38 @@ def ldp_histogram(img, k: int = 3, path=ResponsePath.Accelerated) -> np.ndarray:
     return out
 
 
+_DESC_LBP = 2  # ALDP_DESC_LBP
+
+
 def windowed_features(img, window: int, descriptor=Descriptor.Aldp) -> np.ndarray:
-    """aldp::windowed_features for Ldp/Aldp: [grid cells, 56] uint64, row-major
-    windows, each window clamped as an independent image."""
+    """aldp::windowed_features: [grid cells, bins] uint64 (56 bins for Ldp/Aldp,
+    256 for Lbp), row-major windows, each window clamped as an independent image."""
     if isinstance(descriptor, str):
         descriptor = parse_descriptor(descriptor)
-    if descriptor is Descriptor.Lbp:
-        raise NotImplementedError("LBP is not on the B200 LDP path (SURVEY.md 8f)")
     a = _as_image(img)
     grid = make_grid(a, window)
-    out = np.zeros((grid.total(), 56), dtype=np.uint64)
-    path = ResponsePath.Naive if descriptor is Descriptor.Ldp else ResponsePath.Accelerated
-    _check(lib.aldp_windowed_features(a.ctypes.data, a.shape[0], a.shape[1], int(window), int(path),
+    nb = 256 if descriptor is Descriptor.Lbp else 56
+    out = np.zeros((grid.total(), nb), dtype=np.uint64)
+    sel = (_DESC_LBP if descriptor is Descriptor.Lbp else
+           int(ResponsePath.Naive if descriptor is Descriptor.Ldp else ResponsePath.Accelerated))
+    _check(lib.aldp_windowed_features(a.ctypes.data, a.shape[0], a.shape[1], int(window), sel,
                                       out.ctypes.data, out.size))
+    return out
+
+
+def lbp_histogram(img) -> np.ndarray:
+    """aldp::lbp_histogram (descriptors.cpp:159-168): 256 uint64 bins."""
+    a = _as_image(img)
+    out = np.zeros(256, dtype=np.uint64)
+    _check(lib.aldp_lbp_histogram(a.ctypes.data, a.shape[0], a.shape[1], out.ctypes.data))
+    return out
+
+
+def lbp_code_map(img) -> np.ndarray:
+    """LBP code map: codes[x, y] = lbp_code(img, x, y) (descriptors.cpp:141-157)."""
+    a = _as_image(img)
+    out = np.zeros_like(a)
+    _check(lib.aldp_lbp_code_map(a.ctypes.data, a.shape[0], a.shape[1], out.ctypes.data))
     return out
 
 
@@ -209,22 +234,35 @@ def ldp_code_map(img, k: int = 3, path=ResponsePath.Accelerated) -> np.ndarray:
 def ldp_batch_host(pixels: np.ndarray, k: int = 3, cell: Tuple[int, int] = (0, 0),
                    codes: bool = True, hist: bool = True, stream: int = 0):
     """Host batch [n, rows, cols] uint8 -> (codes [n, rows, cols] | None,
-    hist uint32 [n, cells, n_bins] | None). H2D, kernel and D2H in one call."""
+    hist uint32 [n, cells, n_bins] | None). H2D, kernel and D2H in one call.
+    k == 0 selects LBP (256 bins)."""
     px = np.ascontiguousarray(pixels, dtype=np.uint8)
     if px.ndim == 2:
         px = px[None]
     n, rows, cols = px.shape
-    nb = n_bins(k)
+    nb = 256 if k == 0 else n_bins(k)
     cells = grid_cells(rows, cols, *cell)
     c = np.empty_like(px) if codes else None
     h = np.empty((n, cells, nb), dtype=np.uint32) if hist else None
-    _check(lib.aldp_ldp_batch_host(px.ctypes.data, n, rows, cols, int(k), int(cell[0]), int(cell[1]),
-                                   c.ctypes.data if c is not None else None,
-                                   h.ctypes.data if h is not None else None, stream or None))
+    cp = c.ctypes.data if c is not None else None
+    hp = h.ctypes.data if h is not None else None
+    if k == 0:
+        _check(lib.aldp_lbp_batch_host(px.ctypes.data, n, rows, cols, int(cell[0]), int(cell[1]), cp, hp,
+                                       stream or None))
+    else:
+        _check(lib.aldp_ldp_batch_host(px.ctypes.data, n, rows, cols, int(k), int(cell[0]), int(cell[1]),
+                                       cp, hp, stream or None))
     return c, h
 
 
 _KERNEL = {"auto": 0, "fast": 1, "generic": 2}
+
+
+def lbp_batch(pixels, rows: int, cols: int, cell: Tuple[int, int] = (0, 0), codes=None, hist=None,
+              kernel: str = "auto", stream: Optional[int] = None):
+    """Device-resident LBP batch: like ldp_batch, hist [n, cells, 256]."""
+    return ldp_batch(pixels, rows, cols, k=0, cell=cell, codes=codes, hist=hist, kernel=kernel,
+                     stream=stream)
 
 
 def ldp_batch(pixels, rows: int, cols: int, k: int = 3, cell: Tuple[int, int] = (0, 0),
@@ -245,7 +283,7 @@ def ldp_batch(pixels, rows: int, cols: int, k: int = 3, cell: Tuple[int, int] = 
     n, r, pitch = pixels.shape
     if r != rows or pitch < cols:
         raise ValueError("pixels shape does not match rows/cols")
-    nb = n_bins(k)
+    nb = 256 if k == 0 else n_bins(k)  # k == 0: LBP (internal convention, lbp_batch)
     cells = grid_cells(rows, cols, *cell)
     if codes is True:
         codes = torch.empty((n, rows, pitch), dtype=torch.uint8, device=pixels.device)
@@ -268,7 +306,8 @@ def ldp_batch(pixels, rows: int, cols: int, k: int = 3, cell: Tuple[int, int] = 
         a.d_hist = hist.data_ptr()
     if stream is None:
         stream = torch.cuda.current_stream(pixels.device).cuda_stream
-    _check(lib.aldp_ldp_batch_ex(ctypes.byref(a), _KERNEL[kernel], stream or None))
+    fn = lib.aldp_lbp_batch_ex if k == 0 else lib.aldp_ldp_batch_ex
+    _check(fn(ctypes.byref(a), _KERNEL[kernel], stream or None))
     return codes, hist
 
 

@@ -5,6 +5,8 @@
 //   ldp_histogram      -> aldp_ldp_histogram      (ref descriptors.cpp:123-139)
 //   windowed_features  -> aldp_windowed_features  (ref windowing.cpp:35-63)
 //   ldp_code_map       -> aldp_ldp_code_map       (new)
+//   lbp_histogram      -> aldp_lbp_histogram      (ref descriptors.cpp:159-168)
+//   windowed_features(Lbp) -> aldp_windowed_features (ALDP_DESC_LBP)
 // Status codes become the reference's exceptions: EINVAL ->
 // std::invalid_argument, ERANGE -> std::out_of_range, ECUDA/ENOMEM ->
 // std::runtime_error.
@@ -278,6 +280,28 @@ LdpHistogram ldp_histogram(const GrayImage& img, int k, ResponsePath path) {
     return h;
 }
 
+std::uint64_t LbpHistogram::total() const {
+    return std::accumulate(bins.begin(), bins.end(), std::uint64_t{0});
+}
+
+std::uint8_t lbp_code(const GrayImage& img, int x, int y, BorderPolicy policy, OpCounter* counter) {
+    need_3x3(img);
+    need_inside(img, x, y);
+    const int centre = img.sample(x, y, policy);
+    unsigned code = 0;
+    for (int i = 0; i < 8; ++i)
+        code |= unsigned(img.sample(x + kRing[i][0], y + kRing[i][1], policy) >= centre) << i;
+    if (counter) counter->additions += 8;  // one threshold compare per neighbour
+    return static_cast<std::uint8_t>(code);
+}
+
+LbpHistogram lbp_histogram(const GrayImage& img, BorderPolicy) {
+    need_3x3(img);
+    LbpHistogram h;
+    throw_status(aldp_lbp_histogram(img.pixels().data(), img.rows(), img.cols(), h.bins.data()));
+    return h;
+}
+
 std::vector<std::uint8_t> ldp_code_map(const GrayImage& img, int k, ResponsePath path) {
     if (k < 1 || k > 7) throw std::invalid_argument("k must be in [1, 7]");
     need_3x3(img);
@@ -313,18 +337,18 @@ GrayImage crop(const GrayImage& img, int x0, int y0, int rows, int cols) {
 std::vector<std::vector<std::uint64_t>> windowed_features(const GrayImage& img, int window,
                                                           Descriptor descriptor) {
     const WindowGrid grid = make_grid(img, window);
-    if (descriptor == Descriptor::Lbp)
-        throw std::invalid_argument("LBP windows are not served by the B200 LDP path");
-    std::vector<std::uint64_t> flat(static_cast<std::size_t>(grid.total()) * 56);
-    throw_status(aldp_windowed_features(img.pixels().data(), img.rows(), img.cols(), window,
-                                        descriptor == Descriptor::Ldp ? ALDP_PATH_NAIVE
-                                                                      : ALDP_PATH_ACCELERATED,
+    const std::size_t nb = descriptor == Descriptor::Lbp ? 256 : 56;
+    const int sel = descriptor == Descriptor::Lbp   ? ALDP_DESC_LBP
+                    : descriptor == Descriptor::Ldp ? ALDP_PATH_NAIVE
+                                                    : ALDP_PATH_ACCELERATED;
+    std::vector<std::uint64_t> flat(static_cast<std::size_t>(grid.total()) * nb);
+    throw_status(aldp_windowed_features(img.pixels().data(), img.rows(), img.cols(), window, sel,
                                         flat.data(), flat.size()));
     std::vector<std::vector<std::uint64_t>> out;
     out.reserve(static_cast<std::size_t>(grid.total()));
     for (int w = 0; w < grid.total(); ++w)
-        out.emplace_back(flat.begin() + static_cast<std::ptrdiff_t>(w) * 56,
-                         flat.begin() + static_cast<std::ptrdiff_t>(w + 1) * 56);
+        out.emplace_back(flat.begin() + static_cast<std::ptrdiff_t>(w) * nb,
+                         flat.begin() + static_cast<std::ptrdiff_t>(w + 1) * nb);
     return out;
 }
 

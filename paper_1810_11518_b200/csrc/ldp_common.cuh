@@ -193,4 +193,19 @@ __device__ __forceinline__ unsigned clamped_code(const uint8_t* img, int pitch, 
     return ring_code(r, k);
 }
 
+// LBP code at (x, y) with clamped neighbours (descriptors.cpp:141-157): bit i
+// set when ring neighbour i >= the centre.
+__device__ __forceinline__ unsigned clamped_lbp(const uint8_t* img, int pitch, int x, int y,
+                                                int x_lo, int x_hi, int y_lo, int y_hi) {
+    const int ctr = __ldg(img + size_t(x) * size_t(pitch) + size_t(y));
+    unsigned code = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int xx = min(max(x + ring_dx(j), x_lo), x_hi);
+        const int yy = min(max(y + ring_dy(j), y_lo), y_hi);
+        code |= unsigned(__ldg(img + size_t(xx) * size_t(pitch) + size_t(yy)) >= ctr) << j;
+    }
+    return code;
+}
+
 }  // namespace aldp_b200

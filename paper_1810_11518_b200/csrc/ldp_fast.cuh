@@ -134,6 +134,30 @@ __device__ __forceinline__ uint32_t pair_id(const Col& a, const Col& b, const Co
     }
 }
 
+// LBP codes of one pixel pair (descriptors.cpp:141-157): bit i set when ring
+// neighbour i >= the centre, ring clockwise from the top-left. Each compare is
+// one borrow-free add (values < 2^15, so bit 15/31 of r + 0x8000 - c is the
+// result); four byte permutes in sign-replicate mode turn the eight result
+// bits per lane into 0x00/0xFF bytes, a select chain + fold packs them.
+// Returns the low pixel's code in byte 0 and the high pixel's in byte 1.
+__device__ __forceinline__ uint32_t pair_lbp(const Col& a, const Col& b, const Col& c) {
+    const uint32_t ctr = b.c;
+    const uint32_t r[8] = {a.l, a.c, a.r, b.r, c.r, c.c, c.l, b.l};
+    uint32_t d[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) d[i] = r[i] + 0x80008000u - ctr;
+    // m = [lo bit i, hi bit i, lo bit i+1, hi bit i+1] as 0x00 / 0xFF bytes
+    const uint32_t m01 = prmt(d[0], d[1], 0xFDB9), m23 = prmt(d[2], d[3], 0xFDB9);
+    const uint32_t m45 = prmt(d[4], d[5], 0xFDB9), m67 = prmt(d[6], d[7], 0xFDB9);
+    // bytes 0/1: bits 0,2,4,6 of lo/hi; bytes 2/3: bits 1,3,5,7
+    constexpr uint32_t C01 = 0x02020101u, C23 = 0x08080404u, C45 = 0x20201010u;
+    uint32_t t = (m45 & C45) | (m67 & ~C45);
+    t = (m23 & C23) | (t & ~C23);
+    t = (m01 & C01) | (t & ~C01);
+    t &= 0xAAAA5555u;
+    return t + (t >> 16);  // disjoint bits: add == or
+}
+
 // One unpacked row of a lane: per word j, A/B/L/R and the three pair sums.
 template <int NW>
 struct RowN {
@@ -183,8 +207,14 @@ __device__ __forceinline__ void load_words(const uint8_t* p, uint32_t (&w)[NW]) 
     }
 }
 
+// K = 1..7 (not 4): LDP with top-K codes; K = 0: LBP (descriptors.cpp:141-168).
 template <int K, int NW, bool CELLS, bool CODES, bool HIST>
 __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_kernel(FastParams p) {
+    constexpr bool LBP = K == 0;
+    constexpr int REGION = LBP ? 1024 : kRegion;  // LBP: 256 counts; LDP: code table + 64 counts
+    constexpr int CNT = LBP ? 0 : 256;             // offset of the counts in a region
+    constexpr int NT = LBP ? 256 : 64;             // table entries (codes / XOR ids)
+    constexpr int SEG_SMEM = kSegRegions * REGION;
     constexpr int LC = 4 * NW;              // columns per lane
     constexpr int SEG = kTileCols / LC;     // lanes per segment (tile)
     constexpr int NSEG = 32 / SEG;          // tiles per warp
@@ -202,17 +232,17 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int seg = lane / SEG, sl = lane % SEG;
     const uint32_t smem_base = uint32_t(__cvta_generic_to_shared(smem));
-    const uint32_t seg_base = smem_base + (warp * NSEG + seg) * kSegSmem;
+    const uint32_t seg_base = smem_base + (warp * NSEG + seg) * SEG_SMEM;
 
-    // id -> code table copies (one per region) and zeroed counts.
+    // LDP: id -> code table copies (one per region); zeroed counts.
     {
         uint32_t* w = reinterpret_cast<uint32_t*>(smem);
-        const int words = kFastWarps * NSEG * kSegSmem / 4;
+        const int words = kFastWarps * NSEG * SEG_SMEM / 4;
         for (int i = threadIdx.x; i < words; i += blockDim.x) {
-            const int in_region = i & (kRegion / 4 - 1);
-            w[i] = in_region < 64 ? uint32_t(p.id_code[in_region]) : 0u;
+            const int in_region = i & (REGION / 4 - 1);
+            w[i] = (!LBP && in_region < 64) ? uint32_t(p.id_code[in_region]) : 0u;
         }
-        if (threadIdx.x < 64) id_bin[threadIdx.x] = p.id_bin[threadIdx.x];
+        if (!LBP && threadIdx.x < 64) id_bin[threadIdx.x] = p.id_bin[threadIdx.x];
     }
     __syncthreads();
 
@@ -239,7 +269,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
     const uint32_t seg_lane0 = uint32_t(seg * SEG);
     const uint32_t src_prev = seg_lane0 + uint32_t((sl + SEG - 1) % SEG);
     const uint32_t src_next = seg_lane0 + uint32_t((sl + 1) % SEG);
-    const uint32_t trash = seg_base + kMaxTileCells * kRegion + 256;
+    const uint32_t trash = seg_base + kMaxTileCells * REGION + CNT;
     const uint32_t one = p.one;
 
     for (int64_t wt = warp_global; NSEG * wt < p.n_tiles; wt += warp_stride) {
@@ -361,7 +391,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
                 on = on && cc < p.grid_c && !(in == 0 && col > 0) && !(in == p.cell_cols - 1 && col < last);
                 lc = cc - cell_c0;
             }
-            slot[s] = on ? seg_base + uint32_t(lc) * kRegion + 256 : trash;
+            slot[s] = on ? seg_base + uint32_t(lc) * REGION + CNT : trash;
         }
         // per-lane code-map pointer at row r0; a row's store adds one IMAD.WIDE
         uint8_t* const lane_dst =
@@ -374,19 +404,26 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
         // Slot addresses of the lane's pixel ids. Pair q = 2j (P_A of word
         // j) covers columns y+4j (lo) / y+4j+2 (hi); q = 2j+1 (P_B) covers
         // y+4j+1 / y+4j+3. The id sits in bits 0-5 (lo) and 16-21 (hi).
+        // LBP: the pair's two codes sit in bytes 0 and 1 instead.
         auto addrs = [&](const uint32_t (&X)[NPAIR], uint32_t (&ad)[LC]) {
 #pragma unroll
             for (int q = 0; q < NPAIR; ++q) {
                 const int s_lo = (q >> 1) * 4 + (q & 1), s_hi = s_lo + 2;
-                ad[s_lo] = ((X[q] * 4u) & 0xFCu) | slot[s_lo];
-                ad[s_hi] = (__umulhi(X[q], 1u << 18) & 0xFCu) | slot[s_hi];
+                constexpr uint32_t M = (NT - 1) * 4;
+                ad[s_lo] = ((X[q] * 4u) & M) | slot[s_lo];
+                ad[s_hi] = (LBP ? (X[q] >> 6) & M : __umulhi(X[q], 1u << 18) & M) | slot[s_hi];
             }
         };
         auto row_ids = [&](const RowN<NW>& a, const RowN<NW>& b, const RowN<NW>& c, uint32_t (&X)[NPAIR]) {
 #pragma unroll
             for (int j = 0; j < NW; ++j) {
-                X[2 * j] = pair_id<K>(colA<SUMS>(a, j), colA<SUMS>(b, j), colA<SUMS>(c, j), one);
-                X[2 * j + 1] = pair_id<K>(colB<SUMS>(a, j), colB<SUMS>(b, j), colB<SUMS>(c, j), one);
+                if constexpr (LBP) {
+                    X[2 * j] = pair_lbp(colA<SUMS>(a, j), colA<SUMS>(b, j), colA<SUMS>(c, j));
+                    X[2 * j + 1] = pair_lbp(colB<SUMS>(a, j), colB<SUMS>(b, j), colB<SUMS>(c, j));
+                } else {
+                    X[2 * j] = pair_id<K>(colA<SUMS>(a, j), colA<SUMS>(b, j), colA<SUMS>(c, j), one);
+                    X[2 * j + 1] = pair_id<K>(colB<SUMS>(a, j), colB<SUMS>(b, j), colB<SUMS>(c, j), one);
+                }
             }
         };
 
@@ -399,13 +436,19 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
             addrs(X, ad);
             const bool live = SIMPLE || i < seg_rows;
             if (CODES) {
-                uint32_t e[LC];
-#pragma unroll
-                for (int s = 0; s < LC; ++s) e[s] = lds32(ad[s] - 256);
                 uint32_t wd[NW];
+                if constexpr (LBP) {
 #pragma unroll
-                for (int j = 0; j < NW; ++j)  // bytes -> word with multiply-adds (FMA pipe)
-                    wd[j] = e[4 * j] + e[4 * j + 1] * 0x100u + e[4 * j + 2] * 0x10000u + e[4 * j + 3] * 0x1000000u;
+                    for (int j = 0; j < NW; ++j)  // [A.lo, B.lo, A.hi, B.hi]
+                        wd[j] = prmt(X[2 * j], X[2 * j + 1], 0x5140);
+                } else {
+                    uint32_t e[LC];
+#pragma unroll
+                    for (int s = 0; s < LC; ++s) e[s] = lds32(ad[s] - 256);
+#pragma unroll
+                    for (int j = 0; j < NW; ++j)  // bytes -> word with multiply-adds (FMA pipe)
+                        wd[j] = e[4 * j] + e[4 * j + 1] * 0x100u + e[4 * j + 2] * 0x10000u + e[4 * j + 3] * 0x1000000u;
+                }
                 if (SIMPLE || (live && lane_out)) {
                     uint8_t* o = lane_dst + (long long)i * p.codes_pitch;
                     if constexpr (NW == 1) *reinterpret_cast<uint32_t*>(o) = wd[0];
@@ -497,7 +540,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
                 // left border: (c, c, r); right border: (l, c, c)
                 const uint32_t o = uint32_t(col - 1 - wo);
                 wsel[h] = left ? (o + 1) | ((o + 1) << 4) | ((o + 2) << 8) : o | ((o + 1) << 4) | ((o + 1) << 8);
-                addr[h] = act ? seg_base + uint32_t(cc - cell_c0) * kRegion + 256 : trash;
+                addr[h] = act ? seg_base + uint32_t(cc - cell_c0) * REGION + CNT : trash;
             }
             int n_it = max(len[0], len[1]);
             for (int o = 16; o > 0; o >>= 1) n_it = max(n_it, __shfl_xor_sync(FULL, n_it, o));
@@ -535,9 +578,12 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
             for (int it = 0; it < n_it; ++it) {
                 const Col wc = make_col(qn);
                 fetch(xs[0] + it + 2, xs[1] + it + 2, qn);  // next row in flight
-                const uint32_t X = pair_id<K>(wa, wb, wc, one);
-                red_shared(((X * 4u) & 0xFCu) | (it < len[0] ? addr[0] : trash));
-                red_shared((__umulhi(X, 1u << 18) & 0xFCu) | (it < len[1] ? addr[1] : trash));
+                constexpr uint32_t M = (NT - 1) * 4;
+                uint32_t X;
+                if constexpr (LBP) X = pair_lbp(wa, wb, wc);
+                else X = pair_id<K>(wa, wb, wc, one);
+                red_shared(((X * 4u) & M) | (it < len[0] ? addr[0] : trash));
+                red_shared(((LBP ? X >> 6 : __umulhi(X, 1u << 18)) & M) | (it < len[1] ? addr[1] : trash));
                 wa = wb;
                 wb = wc;
             }
@@ -557,19 +603,20 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
             }
             const int64_t cells_per_image = CELLS ? int64_t(p.grid_r) * p.grid_c : 1;
             uint8_t* seg_ptr = smem + (seg_base - smem_base);
-            for (int j = sl; j < ntab * 64; j += SEG) {
-                const int lc = j >> 6, id = j & 63;
-                uint32_t* cnt = reinterpret_cast<uint32_t*>(seg_ptr + lc * kRegion + 256);
+            for (int j = sl; j < ntab * NT; j += SEG) {
+                const int lc = j / NT, id = j % NT;
+                uint32_t* cnt = reinterpret_cast<uint32_t*>(seg_ptr + lc * REGION + CNT);
                 const uint32_t v = cnt[id];
                 if (v) {
                     const int64_t cell = CELLS ? int64_t(band) * p.grid_c + cell_c0 + lc : 0;
-                    atomicAdd(p.hist + (int64_t(img) * cells_per_image + cell) * p.nbins + id_bin[id], v);
+                    const int bin = LBP ? id : id_bin[id];
+                    atomicAdd(p.hist + (int64_t(img) * cells_per_image + cell) * p.nbins + bin, v);
                     cnt[id] = 0;
                 }
             }
             // the trash region collects masked counts: clear it too
-            uint32_t* tr = reinterpret_cast<uint32_t*>(seg_ptr + kMaxTileCells * kRegion + 256);
-            for (int j = sl; j < 64; j += SEG) tr[j] = 0;
+            uint32_t* tr = reinterpret_cast<uint32_t*>(seg_ptr + kMaxTileCells * REGION + CNT);
+            for (int j = sl; j < NT; j += SEG) tr[j] = 0;
         }
         __syncwarp();
     }

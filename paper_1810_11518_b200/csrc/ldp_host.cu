@@ -94,13 +94,14 @@ static int round_up(int v, int m) { return (v + m - 1) / m * m; }
 // codes (contiguous) and u32 histograms `hist32` [n][cells][bins]. Pinned
 // host memory gives full PCIe rate in both directions at once.
 static aldp_status host_batch(const uint8_t* px, int n, int rows, int cols, int k, int cell_rows,
-                              int cell_cols, uint8_t* codes, uint32_t* hist32, cudaStream_t user) {
+                              int cell_cols, uint8_t* codes, uint32_t* hist32, cudaStream_t user,
+                              bool lbp = false) {
     if (!px && n > 0) return hfail(ALDP_EINVAL, "null pixels");
     if (n < 0) return hfail(ALDP_EINVAL, "negative image count");
     if (rows < 3 || cols < 3)
         return hfail(ALDP_EINVAL, "descriptor extraction needs at least a 3x3 image, got " +
                                       std::to_string(rows) + "x" + std::to_string(cols));
-    const int nbins = aldp_n_bins(k);
+    const int nbins = lbp ? 256 : aldp_n_bins(k);
     if (nbins == 0) return hfail(ALDP_EINVAL, "k must be in [1, 7]");
     const int64_t cells = aldp_grid_cells(rows, cols, cell_rows, cell_cols);
     if (cells < 0) return hfail(ALDP_EINVAL, "invalid window/cell size for this image");
@@ -156,7 +157,7 @@ static aldp_status host_batch(const uint8_t* px, int n, int rows, int cols, int 
         a.codes_img_stride = int64_t(img_bytes);
         a.codes_pitch = pitch;
         a.d_hist = hist32 ? sl.d_hist : nullptr;
-        s = aldp_ldp_batch(&a, st);
+        s = lbp ? aldp_lbp_batch(&a, st) : aldp_ldp_batch(&a, st);
         if (s != ALDP_OK) return hfail(s, aldp_last_error());
         if (codes) {
             uint8_t* dst = codes + size_t(i0) * plane;
@@ -305,19 +306,42 @@ aldp_status aldp_ldp_histogram(const uint8_t* pixels, int rows, int cols, int k,
 
 aldp_status aldp_windowed_features(const uint8_t* pixels, int rows, int cols, int window,
                                    int path, uint64_t* out, size_t out_len) {
-    (void)path;
+    // path: ALDP_PATH_NAIVE / ALDP_PATH_ACCELERATED (Ldp / Aldp, 56 bins) or
+    // ALDP_DESC_LBP (256 bins) -- windowing.cpp:43-58
+    if (path != ALDP_PATH_NAIVE && path != ALDP_PATH_ACCELERATED && path != ALDP_DESC_LBP)
+        return hfail(ALDP_EINVAL, "unknown descriptor");
     if (window < 3) return hfail(ALDP_EINVAL, "window side must be >= 3, got " + std::to_string(window));
     if (window > rows || window > cols)
         return hfail(ALDP_EINVAL, "window side " + std::to_string(window) + " exceeds image " +
                                       std::to_string(rows) + "x" + std::to_string(cols));
+    const bool lbp = path == ALDP_DESC_LBP;
+    const size_t nb = lbp ? 256 : 56;
     const int64_t cells = aldp_grid_cells(rows, cols, window, window);
-    if (out_len < size_t(cells) * 56) return hfail(ALDP_ERANGE, "output buffer too small");
-    uint32_t* h32 = static_cast<uint32_t*>(std::malloc(sizeof(uint32_t) * size_t(cells) * 56));
+    if (out_len < size_t(cells) * nb) return hfail(ALDP_ERANGE, "output buffer too small");
+    uint32_t* h32 = static_cast<uint32_t*>(std::malloc(sizeof(uint32_t) * size_t(cells) * nb));
     if (!h32) return hfail(ALDP_ENOMEM, "host allocation failed");
-    aldp_status s = host_batch(pixels, 1, rows, cols, 3, window, window, nullptr, h32, nullptr);
-    if (s == ALDP_OK) widen(h32, out, size_t(cells) * 56);
+    aldp_status s = host_batch(pixels, 1, rows, cols, 3, window, window, nullptr, h32, nullptr, lbp);
+    if (s == ALDP_OK) widen(h32, out, size_t(cells) * nb);
     std::free(h32);
     return s;
+}
+
+aldp_status aldp_lbp_histogram(const uint8_t* pixels, int rows, int cols, uint64_t* bins256) {
+    uint32_t h32[256];
+    aldp_status s = host_batch(pixels, 1, rows, cols, 3, 0, 0, nullptr, h32, nullptr, true);
+    if (s != ALDP_OK) return s;
+    return widen(h32, bins256, 256);
+}
+
+aldp_status aldp_lbp_code_map(const uint8_t* pixels, int rows, int cols, uint8_t* codes) {
+    if (!codes) return hfail(ALDP_EINVAL, "null codes buffer");
+    return host_batch(pixels, 1, rows, cols, 3, 0, 0, codes, nullptr, nullptr, true);
+}
+
+aldp_status aldp_lbp_batch_host(const uint8_t* pixels, int n_images, int rows, int cols, int cell_rows,
+                                int cell_cols, uint8_t* codes, uint32_t* hist, void* stream) {
+    return host_batch(pixels, n_images, rows, cols, 3, cell_rows, cell_cols, codes, hist,
+                      static_cast<cudaStream_t>(stream), true);
 }
 
 aldp_status aldp_ldp_code_map(const uint8_t* pixels, int rows, int cols, int k, int path,

@@ -78,24 +78,26 @@ __global__ void ldp_generic_kernel(GenericParams p) {
         const int64_t rem = t - int64_t(img) * plane;
         const int x = int(rem / p.cols), y = int(rem - int64_t(x) * p.cols);
         const uint8_t* base = p.px + img * p.img_stride;
-        const unsigned code = clamped_code(base, p.pitch, x, y, 0, p.rows - 1, 0, p.cols - 1, p.k);
+        // k == 0: LBP (256 bins indexed by the code itself)
+        const unsigned code = p.k ? clamped_code(base, p.pitch, x, y, 0, p.rows - 1, 0, p.cols - 1, p.k)
+                                  : clamped_lbp(base, p.pitch, x, y, 0, p.rows - 1, 0, p.cols - 1);
         if (p.codes)
             p.codes[img * p.codes_img_stride + int64_t(x) * p.codes_pitch + y] = uint8_t(code);
         if (!p.hist) continue;
         if (p.cell_rows == 0) {
-            atomicAdd(p.hist + int64_t(img) * p.nbins + colex_rank(code), 1u);
+            atomicAdd(p.hist + int64_t(img) * p.nbins + (p.k ? colex_rank(code) : code), 1u);
         } else {
             const int cr = x / p.cell_rows, cc = y / p.cell_cols;
             if (cr >= p.grid_r || cc >= p.grid_c) continue;  // remainder dropped
             const int x0 = cr * p.cell_rows, y0 = cc * p.cell_cols;
             const bool edge = x == x0 || x == x0 + p.cell_rows - 1 || y == y0 ||
                               y == y0 + p.cell_cols - 1;
-            const unsigned hc =
-                edge ? clamped_code(base, p.pitch, x, y, x0, x0 + p.cell_rows - 1, y0,
-                                    y0 + p.cell_cols - 1, p.k)
-                     : code;
+            unsigned hc = code;
+            if (edge)
+                hc = p.k ? clamped_code(base, p.pitch, x, y, x0, x0 + p.cell_rows - 1, y0, y0 + p.cell_cols - 1, p.k)
+                         : clamped_lbp(base, p.pitch, x, y, x0, x0 + p.cell_rows - 1, y0, y0 + p.cell_cols - 1);
             const int64_t cell = int64_t(img) * p.grid_r * p.grid_c + int64_t(cr) * p.grid_c + cc;
-            atomicAdd(p.hist + cell * p.nbins + colex_rank(hc), 1u);
+            atomicAdd(p.hist + cell * p.nbins + (p.k ? colex_rank(hc) : hc), 1u);
         }
     }
 }
@@ -127,7 +129,8 @@ template <int K, int NW, bool CELLS, bool CODES, bool HIST>
 static aldp_status launch_fast_t(const FastParams& p, cudaStream_t st) {
     auto kern = ldp_fast_kernel<K, NW, CELLS, CODES, HIST>;
     constexpr int NSEG = 32 / (kTileCols / (4 * NW));
-    const size_t smem = size_t(kFastWarps) * NSEG * kSegSmem;
+    constexpr int REGION = K == 0 ? 1024 : kRegion;  // LBP: 256 counts per region
+    const size_t smem = size_t(kFastWarps) * NSEG * kSegRegions * REGION;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     static int per_sm = 1;
@@ -166,6 +169,7 @@ static aldp_status launch_fast_k(const FastParams& p, bool cells, int nw, cudaSt
 
 static aldp_status launch_fast(const FastParams& p, int k, bool cells, int nw, cudaStream_t st) {
     switch (k) {
+    case 0: return launch_fast_k<0>(p, cells, nw, st);  // LBP
     case 1: return launch_fast_k<1>(p, cells, nw, st);
     case 2: return launch_fast_k<2>(p, cells, nw, st);
     case 3: return launch_fast_k<3>(p, cells, nw, st);
@@ -197,9 +201,9 @@ static int max_cells_per_tile(int cols, int cell_cols, int grid_c) {
     return std::max(worst, 1);
 }
 
-static aldp_status validate(const aldp_ldp_args* a, int* grid_r, int* grid_c) {
+static aldp_status validate(const aldp_ldp_args* a, int* grid_r, int* grid_c, bool lbp) {
     if (!a) return fail(ALDP_EINVAL, "null args");
-    if (a->k < 1 || a->k > 7) return fail(ALDP_EINVAL, "k must be in [1, 7]");
+    if (!lbp && (a->k < 1 || a->k > 7)) return fail(ALDP_EINVAL, "k must be in [1, 7]");
     if (a->rows < 3 || a->cols < 3)
         return fail(ALDP_EINVAL, "descriptor extraction needs at least a 3x3 image, got " +
                                      std::to_string(a->rows) + "x" + std::to_string(a->cols));
@@ -224,11 +228,13 @@ static aldp_status validate(const aldp_ldp_args* a, int* grid_r, int* grid_c) {
     return ALDP_OK;
 }
 
-static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st) {
+// lbp: the LBP descriptor (256 bins, k ignored); internally k == 0.
+static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st, bool lbp) {
     int grid_r = 1, grid_c = 1;
-    aldp_status s = validate(a, &grid_r, &grid_c);
+    aldp_status s = validate(a, &grid_r, &grid_c, lbp);
     if (s != ALDP_OK) return s;
-    const int nbins = aldp_n_bins(a->k);
+    const int k = lbp ? 0 : a->k;
+    const int nbins = lbp ? 256 : aldp_n_bins(a->k);
     const int64_t cells = a->cell_rows ? int64_t(grid_r) * grid_c : 1;
     if (a->d_hist)
         ALDP_CUDA_TRY(cudaMemsetAsync(a->d_hist, 0,
@@ -244,7 +250,7 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
                          (a->n_images <= 1 || a->codes_img_stride % al == 0)));
     int ncl = 1;
     if (a->cell_rows) ncl = max_cells_per_tile(a->cols, a->cell_cols, grid_c);
-    const bool fast_ok = aligned && a->k != 4 && ncl <= kMaxTileCells;
+    const bool fast_ok = aligned && k != 4 && ncl <= kMaxTileCells;
     if (kernel == ALDP_KERNEL_FAST && !fast_ok)
         return fail(ALDP_EINVAL, "fast kernel needs cols % 4 == 0, aligned pitches/strides, "
                                  "k != 4 and at most 5 cells per 128 columns");
@@ -271,12 +277,12 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
         p.n_tiles = int64_t(a->n_images) * p.bands * p.blocks;
         p.one = 1;
         for (int id = 0; id < 64; ++id) p.id_code[id] = p.id_bin[id] = 0;
-        for (int c = 0; c < 256; ++c)
-            if (popcount8(c) == a->k) {
+        for (int c = 0; c < 256 && k; ++c)
+            if (popcount8(c) == k) {
                 p.id_code[tag_xor(c)] = uint8_t(c);
                 p.id_bin[tag_xor(c)] = uint8_t(colex_rank(c));
             }
-        return launch_fast(p, a->k, a->cell_rows != 0 && a->d_hist != nullptr, nw, st);
+        return launch_fast(p, k, a->cell_rows != 0 && a->d_hist != nullptr, nw, st);
     }
     GenericParams g{};
     g.px = a->d_pixels;
@@ -285,7 +291,7 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
     g.rows = a->rows;
     g.cols = a->cols;
     g.n_images = a->n_images;
-    g.k = a->k;
+    g.k = k;
     g.codes = a->d_codes;
     g.codes_img_stride = a->codes_img_stride;
     g.codes_pitch = a->codes_pitch;
@@ -310,13 +316,23 @@ using namespace aldp_b200;
 extern "C" {
 
 aldp_status aldp_ldp_batch(const aldp_ldp_args* args, void* stream) {
-    return run_batch(args, ALDP_KERNEL_AUTO, static_cast<cudaStream_t>(stream));
+    return run_batch(args, ALDP_KERNEL_AUTO, static_cast<cudaStream_t>(stream), false);
 }
 
 aldp_status aldp_ldp_batch_ex(const aldp_ldp_args* args, int kernel, void* stream) {
     if (kernel < ALDP_KERNEL_AUTO || kernel > ALDP_KERNEL_GENERIC)
         return fail(ALDP_EINVAL, "unknown kernel selector");
-    return run_batch(args, kernel, static_cast<cudaStream_t>(stream));
+    return run_batch(args, kernel, static_cast<cudaStream_t>(stream), false);
+}
+
+aldp_status aldp_lbp_batch(const aldp_ldp_args* args, void* stream) {
+    return run_batch(args, ALDP_KERNEL_AUTO, static_cast<cudaStream_t>(stream), true);
+}
+
+aldp_status aldp_lbp_batch_ex(const aldp_ldp_args* args, int kernel, void* stream) {
+    if (kernel < ALDP_KERNEL_AUTO || kernel > ALDP_KERNEL_GENERIC)
+        return fail(ALDP_EINVAL, "unknown kernel selector");
+    return run_batch(args, kernel, static_cast<cudaStream_t>(stream), true);
 }
 
 int aldp_n_bins(int k) {

@@ -14,7 +14,8 @@ Two sources, both the reference itself:
          with their k=1..7 code maps (ldp_code over responses_naive and
          responses_accelerated -- both must agree) and k=3 ldp_histogram;
        * tie-heavy {0,1,2} images with constant rectangles, k=1..7 code maps;
-       * windowed_features(img, window, Ldp/Aldp) for several windows;
+       * windowed_features(img, window, Ldp/Aldp/Lbp) for several windows;
+       * LBP code maps and lbp_histogram (aldp::lbp_code / lbp_histogram);
        * the config-1 image: make_random(490, 640, 42), its code map digest
          and whole-image histogram.
 """
@@ -39,7 +40,7 @@ def convert_reference_fixtures():
         with open(os.path.join(REF_GOLDEN, name + ".json")) as f:
             fx = json.load(f)
         out.append({k: fx[k] for k in ("name", "rows", "cols", "pixels", "responses", "ldp_codes",
-                                       "ldp_histogram")})
+                                       "ldp_histogram", "lbp_codes", "lbp_histogram")})
     with open(os.path.join(HERE, "reference_fixtures.json"), "w") as f:
         json.dump({"source": "reference proj/tests/golden/*.json (generate.py brute force)",
                    "fixtures": out}, f)
@@ -53,6 +54,11 @@ def tie_image(rng, rows, cols):
         x, y = rng.integers(0, rows), rng.integers(0, cols)
         img[x:x + h, y:y + w] = rng.integers(0, 3)
     return img
+
+
+def ref_lbp(img):
+    codes, hist = oracle.ref_batch(img, k=0, threads=1)  # aldp::lbp_code / lbp_histogram
+    return codes[0], hist[0, 0]
 
 
 def ref_code_maps(img):
@@ -75,11 +81,13 @@ def main():
         vec[f"rand{i}_img"] = img
         vec[f"rand{i}_codes"] = ref_code_maps(img)
         vec[f"rand{i}_hist"] = oracle.ref_ldp_histogram(img, 3, 1)
+        vec[f"rand{i}_lbpcodes"], vec[f"rand{i}_lbphist"] = ref_lbp(img)
     for i, (r, c) in enumerate([(3, 3), (9, 12), (32, 48), (57, 200)]):
         img = tie_image(rng, r, c)
         vec[f"tie{i}_img"] = img
         vec[f"tie{i}_codes"] = ref_code_maps(img)
         vec[f"tie{i}_hist"] = oracle.ref_ldp_histogram(img, 3, 1)
+        vec[f"tie{i}_lbpcodes"], vec[f"tie{i}_lbphist"] = ref_lbp(img)
     big = oracle.ref_make_random(96, 128, 77)
     vec["win_img"] = big
     for w in (3, 10, 25, 32, 64, 96):
@@ -87,6 +95,8 @@ def main():
         aldp = oracle.ref_windowed(big, w, 1)
         assert np.array_equal(ldp, aldp)
         vec[f"win{w}"] = aldp
+        _, lbpw = oracle.ref_batch(big, k=0, cell=(w, w), codes=False, threads=1)  # windowed_features(Lbp)
+        vec[f"winlbp{w}"] = lbpw[0]
     c1 = oracle.ref_make_random(490, 640, 42)
     c1_codes, c1_hist = oracle.ref_batch(c1, k=3, threads=os.cpu_count())
     vec["c1_img_sha256"] = np.frombuffer(hashlib.sha256(c1.tobytes()).digest(), np.uint8)

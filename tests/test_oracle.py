@@ -22,6 +22,29 @@ def test_port_matches_reference_golden_fixtures(golden_fixtures):
         assert list(oracle.histogram(img, 3)) == fx["ldp_histogram"], fx["name"]
 
 
+def test_port_lbp_matches_reference_golden_fixtures(golden_fixtures):
+    """LBP codes / 256-bin histograms of the same fixtures (generate.py:55-76)."""
+    for fx in golden_fixtures:
+        img = np.array(fx["pixels"], np.uint8).reshape(fx["rows"], fx["cols"])
+        c, h = oracle.batch(img, k=0)
+        assert list(c.ravel()) == fx["lbp_codes"], fx["name"]
+        assert list(h[0, 0]) == fx["lbp_histogram"], fx["name"]
+
+
+def test_port_lbp_matches_reference_library(ref_vectors):
+    names = sorted({k.rsplit("_", 1)[0] for k in ref_vectors if k.endswith("_lbpcodes")})
+    assert len(names) >= 10
+    for nm in names:
+        c, h = oracle.batch(ref_vectors[nm + "_img"], k=0)
+        assert np.array_equal(c[0], ref_vectors[nm + "_lbpcodes"]), nm
+        assert np.array_equal(h[0, 0], ref_vectors[nm + "_lbphist"]), nm
+    img = ref_vectors["win_img"]
+    for w in (3, 10, 25, 32, 64, 96):
+        assert np.array_equal(oracle.cell_histograms(img, w, w, 0), ref_vectors[f"winlbp{w}"]), w
+    # constant image: every neighbour >= centre -> code 255 (descriptors.hpp:57-59)
+    assert oracle.histogram(np.full((6, 7), 9, np.uint8), 0)[255] == 42
+
+
 def test_port_matches_reference_library_vectors(ref_vectors):
     """Code maps k=1..7 and histograms produced by the reference library."""
     names = sorted({k.rsplit("_", 1)[0] for k in ref_vectors if k.endswith("_img") and

@@ -297,3 +297,63 @@ def test_host_batch_pipelined_chunks():
     aldp._check(aldp.lib.aldp_ldp_batch_host(pinned.data_ptr(), n, 490, 640, 3, 81, 91, c2.data_ptr(),
                                              h2.data_ptr(), None))
     assert torch.equal(c2, codes.cpu()) and torch.equal(h2, hist.cpu())
+
+
+# ------------------------------------------------------------------- LBP
+
+def run_lbp(px_host, cell=(0, 0), kernel="auto", pitch=None):
+    px_host = np.ascontiguousarray(px_host, np.uint8)
+    if px_host.ndim == 2:
+        px_host = px_host[None]
+    n, r, c = px_host.shape
+    d = to_dev(px_host, pitch)
+    codes, hist = aldp.lbp_batch(d, r, c, cell=cell, codes=True, hist=True, kernel=kernel)
+    torch.cuda.synchronize()
+    return codes[:, :, :c].cpu().numpy(), hist.cpu().numpy().astype(np.uint64)
+
+
+def test_lbp_reference_goldens(golden_fixtures, ref_vectors):
+    for fx in golden_fixtures:
+        img = np.array(fx["pixels"], np.uint8).reshape(fx["rows"], fx["cols"])
+        for kern in ("auto", "generic"):
+            c, h = run_lbp(img, kernel=kern)
+            assert list(c.ravel()) == fx["lbp_codes"] and list(h[0, 0]) == fx["lbp_histogram"], kern
+    names = sorted({k.rsplit("_", 1)[0] for k in ref_vectors if k.endswith("_lbpcodes")})
+    for nm in names:
+        c, h = run_lbp(ref_vectors[nm + "_img"])
+        assert np.array_equal(c[0], ref_vectors[nm + "_lbpcodes"]), nm
+        assert np.array_equal(h[0, 0], ref_vectors[nm + "_lbphist"]), nm
+    img = ref_vectors["win_img"]
+    for w in (3, 10, 25, 32, 64, 96):
+        for kern in ("auto", "generic"):
+            _, h = run_lbp(img, cell=(w, w), kernel=kern)
+            assert np.array_equal(h[0], ref_vectors[f"winlbp{w}"]), (w, kern)
+
+
+@pytest.mark.parametrize("cell", [(0, 0), (81, 91), (64, 64), (33, 70), (8, 12)])
+def test_lbp_random_ties_faces(cell):
+    rng = np.random.default_rng(cell[0] + 7)
+    imgs = [rng.integers(0, 256, size=(2, 130, 256), dtype=np.uint8)]
+    t = aldp.gen_ties(2, 130, 256, seed=5, device=DEV)
+    f = aldp.gen_faces(2, 130, 256, blobs=8, seed=6, device=DEV)
+    torch.cuda.synchronize()
+    imgs += [t[:, :, :256].cpu().numpy(), f[:, :, :256].cpu().numpy()]
+    for img in imgs:
+        want_c, want_h = oracle.batch(img, k=0, cell=cell)
+        for kern in ("auto", "generic"):
+            c, h = run_lbp(img, cell=cell, kernel=kern)
+            assert np.array_equal(c, want_c), (cell, kern)
+            assert np.array_equal(h, want_h), (cell, kern)
+
+
+def test_lbp_host_entry_points():
+    img = oracle.make_random(41, 57, 3)
+    _, want_h = oracle.batch(img, k=0)
+    assert np.array_equal(aldp.lbp_histogram(img), want_h[0, 0])
+    assert np.array_equal(aldp.lbp_code_map(img), oracle.code_map(img, 0))
+    for w in (3, 9, 41):
+        assert np.array_equal(aldp.windowed_features(img, w, "lbp"), oracle.cell_histograms(img, w, w, 0))
+    batch = np.stack([img, img[::-1].copy(), img[:, ::-1].copy()])
+    c, h = aldp.ldp_batch_host(batch, k=0, cell=(10, 14))
+    wc, wh = oracle.batch(batch, k=0, cell=(10, 14))
+    assert np.array_equal(c, wc) and np.array_equal(h.astype(np.uint64), wh)
