@@ -46,6 +46,8 @@ CONFIGS = {
     "c1": (1, 490, 640, 3, 0, 0, 0, "random", 42),
     # diagnostic: C5 images with whole-image histograms (cost of the cell grid)
     "c5w": (65536, 490, 640, 3, 0, 0, 20, "faces", 11518),
+    # LBP (k = 0 selects the LBP descriptor) on the C5 batch
+    "c5lbp": (65536, 490, 640, 0, 81, 91, 20, "faces", 11518),
 }
 WORKLOAD_NAMES = {
     "c5": "C5: 65536 x 640x490 face-like, LDP k=3, code map + 7x6 cell histograms",
@@ -54,13 +56,14 @@ WORKLOAD_NAMES = {
     "c3": "C3: 256 x 1024x1024 tie-heavy, LDP k=3, code map + whole-image histograms",
     "c1": "C1: 640x490 uniform random (make_random), LDP k=3, code map + histogram",
     "c5w": "C5 images, whole-image histograms (diagnostic)",
+    "c5lbp": "C5 images, LBP (256-bin) code map + 7x6 cell histograms",
 }
 
 
 def hist_bytes_per_image(rows, cols, k, cr, cc):
     from math import comb
     cells = 1 if cr == 0 else (rows // cr) * (cols // cc)
-    return cells * comb(8, k) * 4
+    return cells * (256 if k == 0 else comb(8, k)) * 4
 
 
 class ClockSampler:
@@ -277,7 +280,7 @@ def main():
             import oracle
             px = torch.from_numpy(oracle.make_random(rows, cols, seed)[None].copy()).to(dev)
         cells = aldp.grid_cells(rows, cols, cr, cc)
-        nb = aldp.n_bins(k)
+        nb = 256 if k == 0 else aldp.n_bins(k)
         codes = torch.empty((mine, rows, pitch), dtype=torch.uint8, device=dev)
         hist = torch.empty((mine, cells, nb), dtype=torch.int32, device=dev)
         gathered = None
@@ -344,7 +347,8 @@ def main():
     achieved = alg_bytes / (launch_ms * 1e-3) / 1e9
 
     line = {
-        "metric": "LDP Mpixel/s (code map + histograms)", "value": round(value, 1), "unit": "Mpixel/s",
+        "metric": ("LBP" if k == 0 else "LDP") + " Mpixel/s (code map + histograms)", "value": round(value, 1),
+        "unit": "Mpixel/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic (device generator, seeded, keyed by global image index)",
@@ -376,8 +380,12 @@ def main():
         hh = torch.empty((e2n, cells, nb), dtype=torch.int32).pin_memory()
 
         def e2e_call():
-            st = aldp.lib.aldp_ldp_batch_host(hp.data_ptr(), e2n, rows, cols, k, cr, cc, hc.data_ptr(),
-                                              hh.data_ptr(), None)
+            if k == 0:
+                st = aldp.lib.aldp_lbp_batch_host(hp.data_ptr(), e2n, rows, cols, cr, cc, hc.data_ptr(),
+                                                  hh.data_ptr(), None)
+            else:
+                st = aldp.lib.aldp_ldp_batch_host(hp.data_ptr(), e2n, rows, cols, k, cr, cc, hc.data_ptr(),
+                                                  hh.data_ptr(), None)
             aldp._check(st)
 
         for _ in range(args.warmup):

@@ -146,9 +146,16 @@ __device__ __forceinline__ uint32_t pair_lbp(const Col& a, const Col& b, const C
     uint32_t d[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) d[i] = r[i] + 0x80008000u - ctr;
-    // m = [lo bit i, hi bit i, lo bit i+1, hi bit i+1] as 0x00 / 0xFF bytes
-    const uint32_t m01 = prmt(d[0], d[1], 0xFDB9), m23 = prmt(d[2], d[3], 0xFDB9);
-    const uint32_t m45 = prmt(d[4], d[5], 0xFDB9), m67 = prmt(d[6], d[7], 0xFDB9);
+    // m = [lo bit i, hi bit i, lo bit i+1, hi bit i+1] as 0x00 / 0xFF bytes:
+    // PTX prmt with selector nibbles 8|byte replicates the selected byte's
+    // sign bit (__byte_perm masks that bit off, hence the inline PTX)
+    auto sgn = [](uint32_t x, uint32_t y) {
+        uint32_t r;
+        asm("prmt.b32 %0, %1, %2, 0xFDB9;" : "=r"(r) : "r"(x), "r"(y));
+        return r;
+    };
+    const uint32_t m01 = sgn(d[0], d[1]), m23 = sgn(d[2], d[3]);
+    const uint32_t m45 = sgn(d[4], d[5]), m67 = sgn(d[6], d[7]);
     // bytes 0/1: bits 0,2,4,6 of lo/hi; bytes 2/3: bits 1,3,5,7
     constexpr uint32_t C01 = 0x02020101u, C23 = 0x08080404u, C45 = 0x20201010u;
     uint32_t t = (m45 & C45) | (m67 & ~C45);
@@ -231,12 +238,17 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int seg = lane / SEG, sl = lane % SEG;
-    const uint32_t smem_base = uint32_t(__cvta_generic_to_shared(smem));
+    // Regions must be REGION-aligned in the shared window: a slot address is
+    // formed as (code * 4) | region, so the region's low bits must be zero.
+    // The host allocates REGION extra bytes for this alignment.
+    const uint32_t raw_base = uint32_t(__cvta_generic_to_shared(smem));
+    const uint32_t smem_base = (raw_base + REGION - 1) & ~uint32_t(REGION - 1);
+    uint8_t* const smem_al = smem + (smem_base - raw_base);
     const uint32_t seg_base = smem_base + (warp * NSEG + seg) * SEG_SMEM;
 
     // LDP: id -> code table copies (one per region); zeroed counts.
     {
-        uint32_t* w = reinterpret_cast<uint32_t*>(smem);
+        uint32_t* w = reinterpret_cast<uint32_t*>(smem_al);
         const int words = kFastWarps * NSEG * SEG_SMEM / 4;
         for (int i = threadIdx.x; i < words; i += blockDim.x) {
             const int in_region = i & (REGION / 4 - 1);
@@ -602,7 +614,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
                 }
             }
             const int64_t cells_per_image = CELLS ? int64_t(p.grid_r) * p.grid_c : 1;
-            uint8_t* seg_ptr = smem + (seg_base - smem_base);
+            uint8_t* seg_ptr = smem_al + (seg_base - smem_base);
             for (int j = sl; j < ntab * NT; j += SEG) {
                 const int lc = j / NT, id = j % NT;
                 uint32_t* cnt = reinterpret_cast<uint32_t*>(seg_ptr + lc * REGION + CNT);

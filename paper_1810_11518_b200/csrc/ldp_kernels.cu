@@ -130,7 +130,7 @@ static aldp_status launch_fast_t(const FastParams& p, cudaStream_t st) {
     auto kern = ldp_fast_kernel<K, NW, CELLS, CODES, HIST>;
     constexpr int NSEG = 32 / (kTileCols / (4 * NW));
     constexpr int REGION = K == 0 ? 1024 : kRegion;  // LBP: 256 counts per region
-    const size_t smem = size_t(kFastWarps) * NSEG * kSegRegions * REGION;
+    const size_t smem = size_t(kFastWarps) * NSEG * kSegRegions * REGION + REGION;  // + alignment slack
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     static int per_sm = 1;

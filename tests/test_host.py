@@ -50,7 +50,8 @@ def test_cpp_api_symbols_exported():
     import paper_1810_11518_b200 as aldp
     out = subprocess.run(["nm", "-DC", aldp.LIB_PATH], capture_output=True, text=True).stdout
     for sym in ("aldp::ldp_histogram(", "aldp::windowed_features(", "aldp::ldp_code_map(",
-                "aldp::ldp_code(", "aldp::ldp_bin_index(", "aldp::make_grid("):
+                "aldp::ldp_code(", "aldp::ldp_bin_index(", "aldp::make_grid(", "aldp::lbp_histogram(",
+                "aldp::lbp_code("):
         assert sym in out, sym
 
 
