@@ -167,7 +167,7 @@ def run_reference(args, cfg_name):
         return 0
     n, rows, cols, k, cr, cc, blobs, gen, seed = CONFIGS[cfg_name]
     threads = os.cpu_count() or 1
-    sample = max(threads * 4, 32) if cfg_name in ("c5", "c2") else 1
+    sample = max(threads * 4, 32) if cfg_name in ("c5", "c2", "c5w", "c5lbp") else 1
     if gen == "faces":
         px = numpy_faces(sample, rows, cols, blobs, seed)
     elif gen == "ties":
@@ -186,15 +186,17 @@ def run_reference(args, cfg_name):
     dt = (time.perf_counter() - t0) / args.steps
     mpx = px.size / dt / 1e6
     line = {
-        "impl": "reference", "metric": "LDP Mpixel/s (code map + histograms)", "value": round(mpx, 3),
+        "impl": "reference", "metric": f"{'LBP' if k == 0 else 'LDP'} Mpixel/s (code map + histograms)",
+        "value": round(mpx, 3),
         "unit": "Mpixel/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic (numpy face-like, same recipe)",
         "config": {"workload": WORKLOAD_NAMES[cfg_name], "images_per_step": int(px.shape[0]),
                    "parallelism": f"{threads} host threads over images", "cpu_only": True},
         "cpu_baseline": {"value": round(mpx, 3), "unit": "Mpixel/s", "cores": threads, "kind": kind,
-                         "sample": f"{px.shape[0]} images of {rows}x{cols} per step, ALDP "
-                                   f"(ResponsePath::Accelerated), code map + histograms"},
+                         "sample": f"{px.shape[0]} images of {rows}x{cols} per step, "
+                                   f"{'LBP' if k == 0 else 'ALDP (ResponsePath::Accelerated)'}, "
+                                   f"code map + histograms"},
         "e2e": {"value": round(mpx, 3), "unit": "Mpixel/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }

@@ -143,6 +143,54 @@ aldp_status aldp_ldp_batch_host(const uint8_t* pixels, int n_images, int rows, i
                                 int cell_rows, int cell_cols, uint8_t* codes, uint32_t* hist,
                                 void* stream);
 
+/* ---- response field and the equivalence sweep ---- */
+
+/* Device batch of aldp::response_field (include/aldp/kirsch.hpp:91-92,
+ * src/kirsch.cpp:193-208): d_out is int16 [n][rows][cols][8] (16 B/px,
+ * 16-byte aligned), direction-minor like ResponseVector::m. path selects the
+ * literal masks (ALDP_PATH_NAIVE) or the identity (ALDP_PATH_ACCELERATED);
+ * both give identical values. Clamp borders. Image < 3x3 -> ALDP_EINVAL. */
+aldp_status aldp_response_field_batch(const uint8_t* d_pixels, int64_t img_stride, int rows, int cols,
+                                      int pitch, int n_images, int path, int16_t* d_out, void* stream);
+/* Same, int32 output (the reference's ResponseVector width, 32 B/px). */
+aldp_status aldp_response_field_batch32(const uint8_t* d_pixels, int64_t img_stride, int rows, int cols,
+                                        int pitch, int n_images, int path, int32_t* d_out, void* stream);
+/* Host buffers: out = int32 [rows*cols][8], the reference's
+ * std::vector<ResponseVector> flattened (kirsch.cpp:193-208). */
+aldp_status aldp_response_field(const uint8_t* pixels, int rows, int cols, int path, int32_t* out);
+
+/* aldp::FaultInjection (include/aldp/verify.hpp:14-20): adds delta to column
+ * term term_index (0..14, ColumnTerms::a) at pixel (x, y) of image
+ * image_index before reconstruction. */
+typedef struct {
+    int image_index, x, y, term_index, delta;
+} aldp_fault;
+
+/* aldp::VerifyResult + Mismatch (verify.hpp:22-37), flattened. Counts follow
+ * the reference's bookkeeping for the given thread count (verify.cpp:63-111);
+ * `mismatches` (NEW) is the total number of mismatching (pixel, direction)
+ * pairs the full device sweep saw. */
+typedef struct {
+    uint64_t images_checked, pixels_checked, mismatches;
+    int has_mismatch; /* !VerifyResult::ok() */
+    int image_index, x, y, direction, naive_value, accelerated_value;
+} aldp_verify_result;
+
+/* aldp::verify_equivalence (verify.hpp:43-46): `images` (clamped to >= 1)
+ * seeded random images with sides in [3, 64] derived from `seed` exactly as
+ * the reference does; the sweep runs on the device. fault may be NULL. A
+ * term_index outside [0, 15) -> ALDP_ERANGE. */
+aldp_status aldp_verify_equivalence(int images, uint32_t seed, const aldp_fault* fault, int threads,
+                                    aldp_verify_result* result);
+/* aldp::verify_image (verify.hpp:49-51) on host pixels. */
+aldp_status aldp_verify_image(const uint8_t* pixels, int rows, int cols, const aldp_fault* fault,
+                              int image_index, aldp_verify_result* result);
+/* Device batch of equal-size images (the sweep at scale); `threads` only
+ * shapes the reported counts as in verify_equivalence. */
+aldp_status aldp_verify_batch(const uint8_t* d_pixels, int64_t img_stride, int rows, int cols, int pitch,
+                              int n_images, const aldp_fault* fault, int threads,
+                              aldp_verify_result* result, void* stream);
+
 /* Message for the last non-OK status returned on this host thread. */
 const char* aldp_last_error(void);
 

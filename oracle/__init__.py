@@ -39,6 +39,11 @@ def _load_port():
     L.oracle_histogram.argtypes = [_P, _I, _I, _I, _P]
     L.oracle_cell_histograms.argtypes = [_P, _I, _I, _I, _I, _I, _P]
     L.oracle_batch.argtypes = [_P, _I64, _I, _I, _I, _I, _I, _P, _P, _I]
+    L.oracle_column_terms.argtypes = [_P, _I, _I, _I, _I, _P]
+    L.oracle_responses_terms.argtypes = [_P, _P]
+    L.oracle_response_field.argtypes = [_P, _I, _I, _P]
+    L.oracle_verify_image.argtypes = [_P, _I, _I, _P, _I, _P]
+    L.oracle_verify_equivalence.argtypes = [_I, _U32, _P, _I, _P]
     return L
 
 
@@ -54,6 +59,9 @@ def _load_ref():
     L.ref_batch.argtypes = [_P, _I64, _I, _I, _I, _I, _I, _I, _P, _P, _I]
     L.ref_median_seconds_batch.argtypes = [_P, _I64, _I, _I, _I, _I, _I, _I, _P, _P, _I, _I]
     L.ref_median_seconds_batch.restype = ctypes.c_double
+    L.ref_response_field.argtypes = [_P, _I, _I, _I, _P]
+    L.ref_verify_equivalence.argtypes = [_I, _U32, _P, _I, _P, _P]
+    L.ref_verify_image.argtypes = [_P, _I, _I, _P, _I, _P, _P]
     return L
 
 
@@ -209,3 +217,96 @@ def ref_responses(img, x: int, y: int, path: int = 0) -> np.ndarray:
     if st:
         raise {1: ValueError, 2: IndexError}.get(st, RuntimeError)("reference rejected the call")
     return out
+
+
+# ---- response field / equivalence sweep ----
+class _VR(ctypes.Structure):
+    _fields_ = [("images_checked", ctypes.c_uint64), ("pixels_checked", ctypes.c_uint64),
+                ("has_mismatch", ctypes.c_int), ("image_index", ctypes.c_int), ("x", ctypes.c_int),
+                ("y", ctypes.c_int), ("direction", ctypes.c_int), ("naive_value", ctypes.c_int),
+                ("accelerated_value", ctypes.c_int)]
+
+
+def _fault5(fault):
+    """fault: None or (image_index, x, y, term_index, delta)."""
+    if fault is None:
+        return None, None
+    arr = np.asarray(fault, np.int32)
+    assert arr.shape == (5,)
+    return arr, arr.ctypes.data
+
+
+def _verify_tuple(counts, mm):
+    """(images_checked, pixels_checked, None | (image, x, y, dir, naive, accel))"""
+    m = tuple(int(v) for v in mm[1:7]) if mm[0] else None
+    return int(counts[0]), int(counts[1]), m
+
+
+def column_terms(img, x: int, y: int) -> np.ndarray:
+    a = _img(img)
+    out = np.empty(15, np.int32)
+    port().oracle_column_terms(a.ctypes.data, a.shape[0], a.shape[1], x, y, out.ctypes.data)
+    return out
+
+
+def responses_terms(a15) -> np.ndarray:
+    a = np.ascontiguousarray(a15, np.int32)
+    out = np.empty(8, np.int32)
+    port().oracle_responses_terms(a.ctypes.data, out.ctypes.data)
+    return out
+
+
+def response_field(img) -> np.ndarray:
+    a = _img(img)
+    out = np.empty((a.shape[0] * a.shape[1], 8), np.int32)
+    port().oracle_response_field(a.ctypes.data, a.shape[0], a.shape[1], out.ctypes.data)
+    return out
+
+
+def verify_image(img, fault=None, image_index: int = 0):
+    a = _img(img)
+    keep, fp = _fault5(fault)
+    r = _VR()
+    if port().oracle_verify_image(a.ctypes.data, a.shape[0], a.shape[1], fp, image_index, ctypes.byref(r)):
+        raise IndexError("fault term_index out of range")
+    return _verify_tuple((r.images_checked, r.pixels_checked),
+                         (r.has_mismatch, r.image_index, r.x, r.y, r.direction, r.naive_value,
+                          r.accelerated_value))
+
+
+def verify_equivalence(images: int, seed: int, fault=None, threads: int = 1):
+    keep, fp = _fault5(fault)
+    r = _VR()
+    if port().oracle_verify_equivalence(images, seed, fp, threads, ctypes.byref(r)):
+        raise IndexError("fault term_index out of range")
+    return _verify_tuple((r.images_checked, r.pixels_checked),
+                         (r.has_mismatch, r.image_index, r.x, r.y, r.direction, r.naive_value,
+                          r.accelerated_value))
+
+
+def ref_response_field(img, path: int = 1) -> np.ndarray:
+    a = _img(img)
+    out = np.empty((a.shape[0] * a.shape[1], 8), np.int32)
+    if ref().ref_response_field(a.ctypes.data, a.shape[0], a.shape[1], path, out.ctypes.data):
+        raise ValueError("reference rejected the call")
+    return out
+
+
+def ref_verify_equivalence(images: int, seed: int, fault=None, threads: int = 1):
+    keep, fp = _fault5(fault)
+    counts = np.zeros(2, np.uint64)
+    mm = np.zeros(7, np.int32)
+    if ref().ref_verify_equivalence(images, seed, fp, threads, counts.ctypes.data, mm.ctypes.data):
+        raise RuntimeError("reference verify failed")
+    return _verify_tuple(counts, mm)
+
+
+def ref_verify_image(img, fault=None, image_index: int = 0):
+    a = _img(img)
+    keep, fp = _fault5(fault)
+    counts = np.zeros(2, np.uint64)
+    mm = np.zeros(7, np.int32)
+    if ref().ref_verify_image(a.ctypes.data, a.shape[0], a.shape[1], fp, image_index, counts.ctypes.data,
+                              mm.ctypes.data):
+        raise RuntimeError("reference verify failed")
+    return _verify_tuple(counts, mm)

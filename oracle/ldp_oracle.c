@@ -294,3 +294,116 @@ int oracle_batch(const uint8_t* px, int64_t n, int rows, int cols, int k, int ce
     for (int t = 0; t < threads; ++t) pthread_join(tid[t], NULL);
     return 0;
 }
+
+/* ---- column terms and the equivalence sweep ----
+ * oracle_column_terms      src/kirsch.cpp:86-138 (fifteen signed column
+ *                          partial sums; the centre weight is zero)
+ * oracle_responses_terms   src/kirsch.cpp:140-157 (kResponseTerms: each
+ *                          response is the sum of three column terms)
+ * oracle_verify_image      src/verify.cpp:37-61
+ * oracle_verify_equivalence src/verify.cpp:19-33,63-111 (corpus from one
+ *                          mt19937; threads only shape the chunked
+ *                          bookkeeping, run sequentially here)            */
+
+/* term n: column offset dy and weights for rows x-1, x, x+1 */
+static const int kTermCol[15] = {-1, 0, 1, 0, 1, -1, 1, -1, 1, -1, -1, 0, -1, 1, 1};
+static const int kTermW[15][3] = {
+    {-3, -3, -3}, {-3, 0, -3}, {5, 5, 5},    {5, 0, -3},   {5, 5, -3},
+    {5, -3, -3},  {5, -3, -3}, {5, 5, -3},   {-3, -3, -3}, {5, 5, 5},
+    {-3, 5, 5},   {-3, 0, 5},  {-3, -3, 5},  {-3, -3, 5},  {-3, 5, 5},
+};
+static const int kResponseTerms[8][3] = {{0, 1, 2},  {0, 3, 4},   {5, 3, 6},    {7, 3, 8},
+                                         {9, 1, 8},  {10, 11, 8}, {12, 11, 13}, {0, 11, 14}};
+
+void oracle_column_terms(const uint8_t* px, int rows, int cols, int x, int y, int32_t* a15) {
+    for (int n = 0; n < 15; ++n) {
+        int acc = 0;
+        for (int k = 0; k < 3; ++k)
+            acc += kTermW[n][k] * sample_win(px, cols, 0, 0, rows, cols, x + k - 1, y + kTermCol[n]);
+        a15[n] = acc;
+    }
+}
+
+void oracle_responses_terms(const int32_t* a15, int32_t* out8) {
+    for (int i = 0; i < 8; ++i)
+        out8[i] = a15[kResponseTerms[i][0]] + a15[kResponseTerms[i][1]] + a15[kResponseTerms[i][2]];
+}
+
+typedef struct {
+    uint64_t images_checked, pixels_checked;
+    int has_mismatch, image_index, x, y, direction, naive_value, accelerated_value;
+} oracle_verify_result;
+
+/* fault5 = {image_index, x, y, term_index, delta} or NULL */
+int oracle_verify_image(const uint8_t* px, int rows, int cols, const int* fault5, int image_index,
+                        oracle_verify_result* r) {
+    memset(r, 0, sizeof(*r));
+    if (fault5 && (fault5[3] < 0 || fault5[3] > 14)) return -1;
+    r->images_checked = 1;
+    for (int x = 0; x < rows; ++x)
+        for (int y = 0; y < cols; ++y) {
+            int32_t naive[8], a[15], accel[8];
+            oracle_responses(px, rows, cols, x, y, naive);
+            oracle_column_terms(px, rows, cols, x, y, a);
+            if (fault5 && fault5[0] == image_index && fault5[1] == x && fault5[2] == y)
+                a[fault5[3]] += fault5[4];
+            oracle_responses_terms(a, accel);
+            ++r->pixels_checked;
+            for (int d = 0; d < 8; ++d)
+                if (naive[d] != accel[d]) {
+                    r->has_mismatch = 1;
+                    r->image_index = image_index, r->x = x, r->y = y, r->direction = d;
+                    r->naive_value = naive[d], r->accelerated_value = accel[d];
+                    return 0;
+                }
+        }
+    return 0;
+}
+
+int oracle_verify_equivalence(int images, uint32_t seed, const int* fault5, int threads,
+                              oracle_verify_result* r) {
+    memset(r, 0, sizeof(*r));
+    if (fault5 && (fault5[3] < 0 || fault5[3] > 14)) return -1;
+    if (images < 1) images = 1;
+    int* dims = (int*)malloc(sizeof(int) * 2 * (size_t)images);
+    uint32_t* seeds = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)images);
+    mt19937 s;
+    mt_seed(&s, seed);
+    for (int i = 0; i < images; ++i) {
+        dims[2 * i] = 3 + (int)(mt_next(&s) % 62);
+        dims[2 * i + 1] = 3 + (int)(mt_next(&s) % 62);
+        seeds[i] = mt_next(&s);
+    }
+    if (threads < 1) threads = 1;
+    if (threads > images) threads = images;
+    const int chunk = (images + threads - 1) / threads;
+    uint8_t* img = (uint8_t*)malloc(64 * 64);
+    for (int t = 0; t < threads; ++t) {
+        const int lo = t * chunk, hi = lo + chunk < images ? lo + chunk : images;
+        for (int i = lo; i < hi; ++i) {
+            oracle_make_random(dims[2 * i], dims[2 * i + 1], seeds[i], img);
+            oracle_verify_result one;
+            oracle_verify_image(img, dims[2 * i], dims[2 * i + 1], fault5, i, &one);
+            r->images_checked += one.images_checked;
+            r->pixels_checked += one.pixels_checked;
+            if (one.has_mismatch) {
+                if (!r->has_mismatch) {
+                    const uint64_t ic = r->images_checked, pc = r->pixels_checked;
+                    *r = one;
+                    r->images_checked = ic, r->pixels_checked = pc;
+                }
+                break;
+            }
+        }
+    }
+    free(img);
+    free(seeds);
+    free(dims);
+    return 0;
+}
+
+/* kirsch.cpp:193-208: the naive responses of every pixel, [rows*cols][8]. */
+void oracle_response_field(const uint8_t* px, int rows, int cols, int32_t* out) {
+    for (int x = 0; x < rows; ++x)
+        for (int y = 0; y < cols; ++y) oracle_responses(px, rows, cols, x, y, out + ((size_t)x * cols + y) * 8);
+}

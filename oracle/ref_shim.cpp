@@ -19,6 +19,8 @@
 //                        the composition windowed_features performs per window)
 //   k == 0 selects LBP: aldp::lbp_code / aldp::lbp_histogram
 //                        (src/descriptors.cpp:141-168), windowed_features(Lbp)
+//   ref_response_field   aldp::response_field             (src/kirsch.cpp:193-208)
+//   ref_verify_*         aldp::verify_equivalence / verify_image (src/verify.cpp:37-111)
 //   ref_batch            the above over a batch, std::thread sharded by image
 //                        (the reference functions are pure)
 #include <cstdint>
@@ -32,6 +34,7 @@
 #include "aldp/descriptors.hpp"
 #include "aldp/image.hpp"
 #include "aldp/kirsch.hpp"
+#include "aldp/verify.hpp"
 #include "aldp/windowing.hpp"
 
 namespace {
@@ -215,6 +218,47 @@ int ref_batch(const uint8_t* px, int64_t n, int rows, int cols, int k, int cell_
     for (int s : status)
         if (s) return s;
     return 0;
+}
+
+// aldp::response_field flattened to int32 [rows*cols][8].
+int ref_response_field(const uint8_t* px, int rows, int cols, int path, int32_t* out) {
+    return guarded([&] {
+        const auto f = aldp::response_field(wrap(px, rows, cols), path_of(path));
+        for (size_t i = 0; i < f.size(); ++i)
+            for (int d = 0; d < 8; ++d) out[i * 8 + d] = f[i].m[d];
+    });
+}
+
+namespace {
+void flatten(const aldp::VerifyResult& v, uint64_t* counts2, int* mm7) {
+    counts2[0] = v.images_checked;
+    counts2[1] = v.pixels_checked;
+    mm7[0] = v.mismatch.has_value();
+    if (v.mismatch) {
+        const aldp::Mismatch& m = *v.mismatch;
+        mm7[1] = m.image_index, mm7[2] = m.x, mm7[3] = m.y, mm7[4] = m.direction;
+        mm7[5] = m.naive_value, mm7[6] = m.accelerated_value;
+    }
+}
+std::optional<aldp::FaultInjection> fault_of(const int* f5) {
+    if (!f5) return std::nullopt;
+    aldp::FaultInjection f;
+    f.image_index = f5[0], f.x = f5[1], f.y = f5[2], f.term_index = f5[3], f.delta = f5[4];
+    return f;
+}
+}  // namespace
+
+// aldp::verify_equivalence; fault5 = {image_index, x, y, term_index, delta} or NULL.
+int ref_verify_equivalence(int images, uint32_t seed, const int* fault5, int threads, uint64_t* counts2,
+                           int* mm7) {
+    return guarded([&] { flatten(aldp::verify_equivalence(images, seed, fault_of(fault5), threads), counts2, mm7); });
+}
+
+int ref_verify_image(const uint8_t* px, int rows, int cols, const int* fault5, int image_index,
+                     uint64_t* counts2, int* mm7) {
+    return guarded([&] {
+        flatten(aldp::verify_image(wrap(px, rows, cols), fault_of(fault5), image_index), counts2, mm7);
+    });
 }
 
 // The reference's own timer (src/bench.cpp:51-78): warm-up pass, batches to

@@ -35,7 +35,8 @@ __all__ = [
     "ResponsePath", "Descriptor", "AldpError", "lib", "LIB_PATH", "n_bins", "grid_cells",
     "WindowGrid", "make_grid", "ldp_histogram", "windowed_features", "ldp_code_map",
     "ldp_batch", "ldp_batch_host", "gen_faces", "gen_ties", "version",
-    "lbp_histogram", "lbp_code_map", "lbp_batch",
+    "lbp_histogram", "lbp_code_map", "lbp_batch", "response_field", "response_field_batch",
+    "FaultInjection", "Mismatch", "VerifyResult", "verify_equivalence", "verify_image", "verify_batch",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -83,6 +84,19 @@ class _Args(ctypes.Structure):
     ]
 
 
+class _Fault(ctypes.Structure):
+    _fields_ = [("image_index", ctypes.c_int), ("x", ctypes.c_int), ("y", ctypes.c_int),
+                ("term_index", ctypes.c_int), ("delta", ctypes.c_int)]
+
+
+class _VerifyResult(ctypes.Structure):
+    _fields_ = [("images_checked", ctypes.c_uint64), ("pixels_checked", ctypes.c_uint64),
+                ("mismatches", ctypes.c_uint64), ("has_mismatch", ctypes.c_int),
+                ("image_index", ctypes.c_int), ("x", ctypes.c_int), ("y", ctypes.c_int),
+                ("direction", ctypes.c_int), ("naive_value", ctypes.c_int),
+                ("accelerated_value", ctypes.c_int)]
+
+
 def _load() -> ctypes.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(
@@ -108,6 +122,14 @@ def _load() -> ctypes.CDLL:
         "aldp_gen_faces": ([P, I, I, I, I, I64, I, U64, I64, P], I),
         "aldp_gen_ties": ([P, I, I, I, I, I64, U64, I64, P], I),
         "aldp_version": ([], ctypes.c_char_p),
+        "aldp_response_field_batch": ([P, I64, I, I, I, I, I, P, P], I),
+        "aldp_response_field_batch32": ([P, I64, I, I, I, I, I, P, P], I),
+        "aldp_response_field": ([P, I, I, I, P], I),
+        "aldp_verify_equivalence": ([I, ctypes.c_uint32, ctypes.POINTER(_Fault), I,
+                                     ctypes.POINTER(_VerifyResult)], I),
+        "aldp_verify_image": ([P, I, I, ctypes.POINTER(_Fault), I, ctypes.POINTER(_VerifyResult)], I),
+        "aldp_verify_batch": ([P, I64, I, I, I, I, ctypes.POINTER(_Fault), I,
+                               ctypes.POINTER(_VerifyResult), P], I),
     }
     for name, (argtypes, restype) in sig.items():
         fn = getattr(L, name)
@@ -344,3 +366,124 @@ def gen_ties(n: int, rows: int, cols: int, seed: int = 11518, first_index: int =
     _check(lib.aldp_gen_ties(out.data_ptr(), n, rows, cols, pitch, rows * pitch, seed, first_index,
                              stream or None))
     return out
+
+
+# ------------------------------------------------------------ response field
+
+def response_field(img, path=ResponsePath.Accelerated) -> np.ndarray:
+    """aldp::response_field (kirsch.hpp:91-92, kirsch.cpp:193-208): int32
+    [rows*cols, 8], the eight signed Kirsch responses per pixel in raster
+    order, computed on the B200."""
+    img = _as_image(img)
+    out = np.empty((img.shape[0] * img.shape[1], 8), np.int32)
+    _check(lib.aldp_response_field(img.ctypes.data, img.shape[0], img.shape[1], _path_value(path),
+                                   out.ctypes.data))
+    return out
+
+
+def response_field_batch(pixels, rows: int, cols: int, path=ResponsePath.Accelerated, out=None,
+                         wide: bool = False, stream: Optional[int] = None):
+    """Device batch: pixels torch.uint8 [n, rows, pitch] -> int16 (or int32
+    when wide) [n, rows, cols, 8]. Asynchronous on the stream."""
+    import torch
+    if pixels.dtype != torch.uint8 or not pixels.is_cuda or pixels.dim() != 3 or not pixels.is_contiguous():
+        raise ValueError("pixels must be a contiguous CUDA uint8 tensor [n, rows, pitch]")
+    n, r, pitch = pixels.shape
+    if r != rows or pitch < cols:
+        raise ValueError("pixels shape does not match rows/cols")
+    dt = torch.int32 if wide else torch.int16
+    if out is None:
+        out = torch.empty((n, rows, cols, 8), dtype=dt, device=pixels.device)
+    if out.dtype != dt or not out.is_contiguous() or out.numel() < n * rows * cols * 8:
+        raise ValueError("out must be a contiguous %s tensor [n, rows, cols, 8]" % dt)
+    if stream is None:
+        stream = torch.cuda.current_stream(pixels.device).cuda_stream
+    fn = lib.aldp_response_field_batch32 if wide else lib.aldp_response_field_batch
+    _check(fn(pixels.data_ptr(), rows * pitch, rows, cols, pitch, n, _path_value(path), out.data_ptr(),
+              stream or None))
+    return out
+
+
+# ------------------------------------------------------------ verification
+
+@dataclass
+class FaultInjection:
+    """aldp::FaultInjection (verify.hpp:14-20)."""
+    image_index: int = 0
+    x: int = 0
+    y: int = 0
+    term_index: int = 0
+    delta: int = 1
+
+
+@dataclass
+class Mismatch:
+    """aldp::Mismatch (verify.hpp:22-29)."""
+    image_index: int = 0
+    x: int = 0
+    y: int = 0
+    direction: int = 0
+    naive_value: int = 0
+    accelerated_value: int = 0
+
+
+@dataclass
+class VerifyResult:
+    """aldp::VerifyResult (verify.hpp:31-37); `mismatches` is new: every
+    mismatching (pixel, direction) the device sweep saw."""
+    images_checked: int = 0
+    pixels_checked: int = 0
+    mismatch: Optional[Mismatch] = None
+    mismatches: int = 0
+
+    def ok(self) -> bool:
+        return self.mismatch is None
+
+
+def _fault_arg(fault: Optional[FaultInjection]):
+    if fault is None:
+        return None
+    return ctypes.byref(_Fault(fault.image_index, fault.x, fault.y, fault.term_index, fault.delta))
+
+
+def _result(r: _VerifyResult) -> VerifyResult:
+    mm = None
+    if r.has_mismatch:
+        mm = Mismatch(r.image_index, r.x, r.y, r.direction, r.naive_value, r.accelerated_value)
+    return VerifyResult(int(r.images_checked), int(r.pixels_checked), mm, int(r.mismatches))
+
+
+def verify_equivalence(images: int, seed: int, fault: Optional[FaultInjection] = None,
+                       threads: int = 1) -> VerifyResult:
+    """aldp::verify_equivalence (verify.hpp:43-46): the naive-vs-accelerated
+    sweep over the reference's seeded corpus, run on the B200."""
+    r = _VerifyResult()
+    _check(lib.aldp_verify_equivalence(int(images), int(seed) & 0xFFFFFFFF, _fault_arg(fault),
+                                       int(threads), ctypes.byref(r)))
+    return _result(r)
+
+
+def verify_image(img, fault: Optional[FaultInjection] = None, image_index: int = 0) -> VerifyResult:
+    """aldp::verify_image (verify.hpp:49-51)."""
+    img = _as_image(img)
+    r = _VerifyResult()
+    _check(lib.aldp_verify_image(img.ctypes.data, img.shape[0], img.shape[1], _fault_arg(fault),
+                                 int(image_index), ctypes.byref(r)))
+    return _result(r)
+
+
+def verify_batch(pixels, rows: int, cols: int, fault: Optional[FaultInjection] = None, threads: int = 1,
+                 stream: Optional[int] = None) -> VerifyResult:
+    """The sweep over a device batch torch.uint8 [n, rows, pitch] (synchronous)."""
+    import torch
+    if pixels.dtype != torch.uint8 or not pixels.is_cuda or pixels.dim() != 3 or not pixels.is_contiguous():
+        raise ValueError("pixels must be a contiguous CUDA uint8 tensor [n, rows, pitch]")
+    n, r_, pitch = pixels.shape
+    if r_ != rows or pitch < cols:
+        raise ValueError("pixels shape does not match rows/cols")
+    if stream is None:
+        stream = torch.cuda.current_stream(pixels.device).cuda_stream
+    r = _VerifyResult()
+    _check(lib.aldp_verify_batch(pixels.data_ptr(), rows * pitch, rows, cols, pitch, n, _fault_arg(fault),
+                                 int(threads), ctypes.byref(r), stream or None))
+    return _result(r)

@@ -7,6 +7,9 @@
 //   ldp_code_map       -> aldp_ldp_code_map       (new)
 //   lbp_histogram      -> aldp_lbp_histogram      (ref descriptors.cpp:159-168)
 //   windowed_features(Lbp) -> aldp_windowed_features (ALDP_DESC_LBP)
+//   response_field     -> aldp_response_field     (ref kirsch.cpp:193-208)
+//   verify_equivalence -> aldp_verify_equivalence (ref verify.cpp:63-111)
+//   verify_image       -> aldp_verify_image       (ref verify.cpp:37-61)
 // Status codes become the reference's exceptions: EINVAL ->
 // std::invalid_argument, ERANGE -> std::out_of_range, ECUDA/ENOMEM ->
 // std::runtime_error.
@@ -25,6 +28,7 @@
 #include "aldp/descriptors.hpp"
 #include "aldp/image.hpp"
 #include "aldp/kirsch.hpp"
+#include "aldp/verify.hpp"
 #include "aldp/windowing.hpp"
 #include "aldp_cuda.h"
 
@@ -213,16 +217,13 @@ ResponseVector responses_accelerated(const ColumnTerms& terms, OpCounter* counte
     return out;
 }
 
-std::vector<ResponseVector> response_field(const GrayImage& img, ResponsePath path,
-                                           BorderPolicy policy) {
+std::vector<ResponseVector> response_field(const GrayImage& img, ResponsePath path, BorderPolicy) {
     need_3x3(img);
-    std::vector<ResponseVector> f;
-    f.reserve(img.pixel_count());
-    for (int x = 0; x < img.rows(); ++x)
-        for (int y = 0; y < img.cols(); ++y)
-            f.push_back(path == ResponsePath::Naive
-                            ? responses_naive(img, x, y, policy)
-                            : responses_accelerated(column_terms(img, x, y, policy)));
+    std::vector<ResponseVector> f(img.pixel_count());
+    static_assert(sizeof(ResponseVector) == 8 * sizeof(std::int32_t), "ResponseVector is int m[8]");
+    throw_status(aldp_response_field(img.pixels().data(), img.rows(), img.cols(),
+                                     path == ResponsePath::Naive ? ALDP_PATH_NAIVE : ALDP_PATH_ACCELERATED,
+                                     reinterpret_cast<std::int32_t*>(f.data())));
     return f;
 }
 
@@ -350,6 +351,36 @@ std::vector<std::vector<std::uint64_t>> windowed_features(const GrayImage& img, 
         out.emplace_back(flat.begin() + static_cast<std::ptrdiff_t>(w) * nb,
                          flat.begin() + static_cast<std::ptrdiff_t>(w + 1) * nb);
     return out;
+}
+
+// ---------------------------------------------------------------- verify
+namespace {
+VerifyResult from_c(const aldp_verify_result& r) {
+    VerifyResult v;
+    v.images_checked = r.images_checked;
+    v.pixels_checked = r.pixels_checked;
+    if (r.has_mismatch)
+        v.mismatch = Mismatch{r.image_index, r.x, r.y, r.direction, r.naive_value, r.accelerated_value};
+    return v;
+}
+aldp_fault to_c(const FaultInjection& f) { return aldp_fault{f.image_index, f.x, f.y, f.term_index, f.delta}; }
+}  // namespace
+
+VerifyResult verify_equivalence(int images, std::uint32_t seed, std::optional<FaultInjection> fault,
+                                int threads) {
+    aldp_verify_result r{};
+    const aldp_fault f = fault ? to_c(*fault) : aldp_fault{};
+    throw_status(aldp_verify_equivalence(images, seed, fault ? &f : nullptr, threads, &r));
+    return from_c(r);
+}
+
+VerifyResult verify_image(const GrayImage& img, std::optional<FaultInjection> fault, int image_index) {
+    need_3x3(img);
+    aldp_verify_result r{};
+    const aldp_fault f = fault ? to_c(*fault) : aldp_fault{};
+    throw_status(aldp_verify_image(img.pixels().data(), img.rows(), img.cols(), fault ? &f : nullptr,
+                                   image_index, &r));
+    return from_c(r);
 }
 
 }  // namespace aldp

@@ -1,0 +1,795 @@
+// ldp_field.cu -- SURVEY 8f rank 2: the raw Kirsch response field on the
+// B200, and the naive-vs-identity equivalence sweep as a device kernel.
+//
+//  * response_field_kernel<NAIVE, OutT>: the eight signed responses of every
+//    pixel (reference response_field, kirsch.cpp:193-208), dense
+//    [n][rows][cols][8] in int16 (16 B/px; |m| <= 3825, test_kirsch.cpp:
+//    288-315) or int32 (the reference's ResponseVector layout). NAIVE = the
+//    literal 3x3 masks (kirsch.cpp:10-29,63-84); otherwise the identity
+//    m_i = 8*S_i - 3*T (ldp_common.cuh). Clamp-to-edge borders. 32x128
+//    tiles staged in shared memory, one thread per column sliding down the
+//    tile, so each warp stores 32 adjacent pixels' vectors (512 contiguous
+//    bytes): 1 B read + 16 B (or 32 B) written per pixel, HBM-bound.
+//  * verify_kernel: verify_image / verify_equivalence (verify.cpp:37-111):
+//    naive masks against the reference's column-term reconstruction
+//    (kirsch.cpp:86-157; expressed through the identity, since
+//    a[t1]+a[t2]+a[t3] == 8*S_i - 3*T exactly), recording per image the
+//    first mismatch in the reference's sweep order (row, column, direction).
+//    An optional fault adds `delta` to column term `term_index` at one pixel,
+//    i.e. to every response that uses that term (kResponseTerms,
+//    kirsch.cpp:142-144), so the failure path runs end to end. The host side
+//    turns the per-image first mismatches into the reference's
+//    VerifyResult for any thread count.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <random>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "aldp_cuda.h"
+
+namespace aldp_b200 {
+
+aldp_status set_error(aldp_status s, const std::string& msg);  // ldp_kernels.cu
+
+#define FIELD_CUDA_TRY(expr)                                                                \
+    do {                                                                                    \
+        cudaError_t _e = (expr);                                                            \
+        if (_e != cudaSuccess)                                                              \
+            return set_error(_e == cudaErrorMemoryAllocation ? ALDP_ENOMEM : ALDP_ECUDA,    \
+                             std::string(#expr) + ": " + cudaGetErrorString(_e));           \
+    } while (0)
+
+// Which responses use column term t (kResponseTerms, kirsch.cpp:142-144): bit i.
+__constant__ uint8_t c_term_users[15] = {
+    0x83, 0x11, 0x01, 0x0E, 0x02, 0x04, 0x04, 0x08, 0x38, 0x10, 0x20, 0xE0, 0x40, 0x40, 0x80,
+};
+
+// ring slot j (clockwise from the top-left, kirsch.cpp:11-12); mask i weights
+// ring slot j with kBase[(i + j) & 7]
+__device__ __forceinline__ void naive8(const int (&r)[8], int (&m)[8]) {
+    constexpr int kBase[8] = {-3, -3, 5, 5, 5, -3, -3, -3};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        int acc = 0;  // the centre weight is zero (kirsch.cpp:63-84)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc += kBase[(i + j) & 7] * r[j];
+        m[i] = acc;
+    }
+}
+
+__device__ __forceinline__ void identity8(const int (&r)[8], int (&m)[8]) {
+    const int t = r[0] + r[1] + r[2] + r[3] + r[4] + r[5] + r[6] + r[7];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) m[i] = 8 * (r[(2 - i) & 7] + r[(3 - i) & 7] + r[(4 - i) & 7]) - 3 * t;
+}
+
+__device__ __forceinline__ uint32_t pk16(int lo, int hi) {
+    return uint32_t(uint16_t(lo)) | (uint32_t(uint16_t(hi)) << 16);
+}
+
+// Tile = kFieldRows rows x kFieldCols columns of one image, one thread per
+// column. The (rows+2) x (cols+2) clamped halo is staged in shared memory
+// first (every thread issues its ~34 independent byte loads back to back, so
+// the tile's reads are all in flight at once), then each thread slides down
+// its column and stores one 16 B (or 32 B) vector per pixel: a warp writes
+// 32 adjacent pixels = 512 contiguous bytes per row.
+constexpr int kFieldCols = 128;
+constexpr int kFieldRows = 32;
+constexpr int kFieldPitch = kFieldCols + 4;
+
+// Grid-stride loop over tiles; stages each tile's clamped halo, then calls
+// body(img, x0, y0, h, w, a/b registers...) per column thread via `column`.
+template <typename Column>
+__device__ __forceinline__ void for_each_tile(const uint8_t* __restrict__ px, int64_t img_stride, int pitch,
+                                              int rows, int cols, int n_images,
+                                              uint8_t (&tile)[kFieldRows + 2][kFieldPitch], Column column) {
+    const int tiles_x = (cols + kFieldCols - 1) / kFieldCols;
+    const int bands = (rows + kFieldRows - 1) / kFieldRows;
+    const int64_t total = int64_t(n_images) * bands * tiles_x;
+    const int tid = threadIdx.x;
+    for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+        const int tx = int(t % tiles_x);
+        const int64_t rest = t / tiles_x;
+        const int band = int(rest % bands), img = int(rest / bands);
+        const int y0 = tx * kFieldCols, x0 = band * kFieldRows;
+        const int h = min(kFieldRows, rows - x0), w = min(kFieldCols, cols - y0);
+        const uint8_t* base = px + img * img_stride;
+        __syncthreads();  // the previous tile's readers are done
+        {
+            // halo column c (0..w+1) <- image column clamp(y0 - 1 + c)
+            const int c0 = tid, c1 = tid + kFieldCols;
+            const int g0 = min(max(y0 - 1 + c0, 0), cols - 1), g1 = min(max(y0 - 1 + c1, 0), cols - 1);
+            const bool has0 = c0 < w + 2, has1 = c1 < w + 2;
+#pragma unroll
+            for (int r = 0; r < kFieldRows + 2; ++r) {
+                if (r < h + 2) {
+                    const uint8_t* row = base + int64_t(min(max(x0 - 1 + r, 0), rows - 1)) * pitch;
+                    if (has0) tile[r][c0] = __ldg(row + g0);
+                    if (has1) tile[r][c1] = __ldg(row + g1);
+                }
+            }
+        }
+        __syncthreads();
+        if (tid < w) column(img, x0, y0 + tid, h);
+    }
+}
+
+// Slides one thread down column tid of the staged tile: f(r, ring) per row.
+template <typename F>
+__device__ __forceinline__ void slide(const uint8_t (&tile)[kFieldRows + 2][kFieldPitch], int h, F f) {
+    const int tid = threadIdx.x;
+    int a0 = tile[0][tid], a1 = tile[0][tid + 1], a2 = tile[0][tid + 2];
+    int b0 = tile[1][tid], b1 = tile[1][tid + 1], b2 = tile[1][tid + 2];
+#pragma unroll 4
+    for (int r = 0; r < h; ++r) {
+        const int c0 = tile[r + 2][tid], c1 = tile[r + 2][tid + 1], c2 = tile[r + 2][tid + 2];
+        const int ring[8] = {a0, a1, a2, b2, c2, c1, c0, b0};
+        f(r, ring);
+        a0 = b0, a1 = b1, a2 = b2;
+        b0 = c0, b1 = c1, b2 = c2;
+    }
+}
+
+template <bool NAIVE, typename OutT>
+__global__ void __launch_bounds__(kFieldCols) response_field_kernel(const uint8_t* __restrict__ px,
+                                                                    int64_t img_stride, int pitch, int rows,
+                                                                    int cols, int n_images,
+                                                                    OutT* __restrict__ out) {
+    __shared__ uint8_t tile[kFieldRows + 2][kFieldPitch];
+    for_each_tile(px, img_stride, pitch, rows, cols, n_images, tile, [&](int img, int x0, int y, int h) {
+        OutT* o = out + ((int64_t(img) * rows + x0) * cols + y) * 8;
+        slide(tile, h, [&](int r, const int (&ring)[8]) {
+            int m[8];
+            if constexpr (NAIVE) naive8(ring, m);
+            else identity8(ring, m);
+            OutT* p = o + int64_t(r) * cols * 8;
+            if constexpr (sizeof(OutT) == 2) {
+                *reinterpret_cast<uint4*>(p) =
+                    make_uint4(pk16(m[0], m[1]), pk16(m[2], m[3]), pk16(m[4], m[5]), pk16(m[6], m[7]));
+            } else {
+                reinterpret_cast<int4*>(p)[0] = make_int4(m[0], m[1], m[2], m[3]);
+                reinterpret_cast<int4*>(p)[1] = make_int4(m[4], m[5], m[6], m[7]);
+            }
+        });
+    });
+}
+
+// ---- bulk-copy (TMA 1D) staged row kernel -----------------------------
+// When rows are 16-byte aligned (pitch, img_stride and base % 16 == 0), a
+// tile is kRowBand rows x the full image width (up to kRowChunk columns), so
+// one tile's output is a single contiguous run of kRowBand*cols*16 bytes.
+// One elected thread streams the tile's kRowBand+2 halo rows into shared
+// memory with cp.async.bulk (the TMA engine; completion counted on an
+// mbarrier), double buffered: tile i+1's rows are in flight while the block
+// computes and stores tile i, so no warp waits on a global load. Each thread
+// owns four columns strided by the block size (four independent pixels per
+// row for latency hiding; each store instruction still writes 32 adjacent
+// pixels = 512 contiguous bytes).
+#ifndef ALDP_ROW_BAND
+#define ALDP_ROW_BAND 16
+#endif
+#ifndef ALDP_ROW_COLS
+#define ALDP_ROW_COLS 4
+#endif
+constexpr int kRowBand = ALDP_ROW_BAND;
+constexpr int kRowChunk = 1024;
+constexpr int kRowCols = ALDP_ROW_COLS;  // columns per thread (strided by blockDim.x)
+static_assert(kRowChunk <= kRowCols * 256, "a chunk must fit one block of <= 256 threads");
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+struct RowTile {
+    int img, x0, y0, h, w;
+};
+
+__device__ __forceinline__ RowTile row_tile(int64_t t, int rows, int cols) {
+    const int chunks = (cols + kRowChunk - 1) / kRowChunk;
+    const int bands = (rows + kRowBand - 1) / kRowBand;
+    const int tx = int(t % chunks);
+    const int64_t rest = t / chunks;
+    RowTile g;
+    g.img = int(rest / bands);
+    g.x0 = int(rest % bands) * kRowBand;
+    g.y0 = tx * kRowChunk;
+    g.h = min(kRowBand, rows - g.x0);
+    g.w = min(kRowChunk, cols - g.y0);
+    return g;
+}
+
+// Shared column of image column c is c - (y0 - 16). One thread arms the
+// buffer's barrier and issues the tile's h+2 row copies (16 B granular).
+__device__ __forceinline__ void issue_row_tile(const uint8_t* px, int64_t img_stride, int pitch, int rows,
+                                               const RowTile& g, uint8_t* buf, int stride, uint64_t* bar) {
+    const int start = max(g.y0 - 16, 0);
+    const int end = min((g.y0 + g.w + 16 + 15) & ~15, pitch);
+    const uint32_t bytes = uint32_t(end - start);
+    const int dst0 = start - (g.y0 - 16);
+    mbar_expect_tx(bar, bytes * uint32_t(g.h + 2));
+    const uint8_t* base = px + g.img * img_stride + start;
+    for (int r = 0; r < g.h + 2; ++r) {
+        const int sx = min(max(g.x0 - 1 + r, 0), rows - 1);
+        bulk_g2s(buf + r * stride + dst0, base + int64_t(sx) * pitch, bytes, bar);
+    }
+}
+
+template <bool NAIVE, typename OutT>
+__global__ void __launch_bounds__(256) response_field_row_kernel(const uint8_t* __restrict__ px,
+                                                                 int64_t img_stride, int pitch, int rows,
+                                                                 int cols, int n_images, int stride,
+                                                                 OutT* __restrict__ out) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ __align__(8) uint64_t full[2];
+    const int chunks = (cols + kRowChunk - 1) / kRowChunk;
+    const int bands = (rows + kRowBand - 1) / kRowBand;
+    const int64_t total = int64_t(n_images) * bands * chunks;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int buf_bytes = (kRowBand + 2) * stride;
+    if (tid == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int b = 0; b < 2; ++b) {
+            const int64_t t = blockIdx.x + int64_t(b) * gridDim.x;
+            if (t < total)
+                issue_row_tile(px, img_stride, pitch, rows, row_tile(t, rows, cols), smem + b * buf_bytes, stride,
+                               &full[b]);
+        }
+    }
+    int i = 0;
+    for (int64_t t = blockIdx.x; t < total; t += gridDim.x, ++i) {
+        const int b = i & 1;
+        const RowTile g = row_tile(t, rows, cols);
+        mbar_wait(&full[b], uint32_t((i >> 1) & 1));
+        // this thread's columns: y0 + tid + k*nt, k < kRowCols (warp-consecutive
+        // pixels per k, so every 16 B store instruction writes 512 contiguous B)
+        const uint8_t* s = smem + b * buf_bytes;
+        int cl[kRowCols], cm[kRowCols], cr[kRowCols];
+        bool ok[kRowCols];
+        int A[kRowCols][3], B[kRowCols][3];
+#pragma unroll
+        for (int k = 0; k < kRowCols; ++k) {
+            const int yl = tid + k * nt;
+            ok[k] = yl < g.w;
+            const int y = g.y0 + min(yl, g.w - 1);
+            cl[k] = max(y - 1, 0) - (g.y0 - 16);
+            cm[k] = y - (g.y0 - 16);
+            cr[k] = min(y + 1, cols - 1) - (g.y0 - 16);
+            A[k][0] = s[cl[k]], A[k][1] = s[cm[k]], A[k][2] = s[cr[k]];
+            B[k][0] = s[stride + cl[k]], B[k][1] = s[stride + cm[k]], B[k][2] = s[stride + cr[k]];
+        }
+        OutT* o = out + ((int64_t(g.img) * rows + g.x0) * cols + g.y0 + tid) * 8;
+        for (int r = 0; r < g.h; ++r, o += int64_t(cols) * 8) {
+            const uint8_t* sr = s + (r + 2) * stride;
+#pragma unroll
+            for (int k = 0; k < kRowCols; ++k) {
+                const int c0 = sr[cl[k]], c1 = sr[cm[k]], c2 = sr[cr[k]];
+                if (ok[k]) {
+                    const int ring[8] = {A[k][0], A[k][1], A[k][2], B[k][2], c2, c1, c0, B[k][0]};
+                    int m[8];
+                    if constexpr (NAIVE) naive8(ring, m);
+                    else identity8(ring, m);
+                    OutT* p = o + int64_t(k) * nt * 8;
+                    if constexpr (sizeof(OutT) == 2) {
+                        *reinterpret_cast<uint4*>(p) = make_uint4(pk16(m[0], m[1]), pk16(m[2], m[3]),
+                                                                  pk16(m[4], m[5]), pk16(m[6], m[7]));
+                    } else {
+                        reinterpret_cast<int4*>(p)[0] = make_int4(m[0], m[1], m[2], m[3]);
+                        reinterpret_cast<int4*>(p)[1] = make_int4(m[4], m[5], m[6], m[7]);
+                    }
+                }
+                A[k][0] = B[k][0], A[k][1] = B[k][1], A[k][2] = B[k][2];
+                B[k][0] = c0, B[k][1] = c1, B[k][2] = c2;
+            }
+        }
+        __syncthreads();  // buffer b fully read
+        if (tid == 0) {
+            const int64_t tn = t + 2 * int64_t(gridDim.x);
+            if (tn < total) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue_row_tile(px, img_stride, pitch, rows, row_tile(tn, rows, cols), smem + b * buf_bytes, stride,
+                               &full[b]);
+            }
+        }
+    }
+}
+
+// Batch geometry for the verify sweep: uniform (img_stride/pitch/rows/cols)
+// or ragged (offsets[n+1] pixel prefix sums of contiguous images, dims[2n]).
+struct VerifyGeom {
+    const uint8_t* px;
+    int64_t img_stride;
+    int pitch, rows, cols, n;
+    const int64_t* offsets;  // ragged when non-null
+    const int32_t* dims;
+};
+
+__device__ __forceinline__ void image_of(const VerifyGeom& g, int img, const uint8_t*& base, int& rows,
+                                         int& cols, int& pitch) {
+    if (!g.offsets) {
+        base = g.px + img * g.img_stride, rows = g.rows, cols = g.cols, pitch = g.pitch;
+    } else {
+        base = g.px + g.offsets[img], rows = g.dims[2 * img], cols = g.dims[2 * img + 1], pitch = cols;
+    }
+}
+
+__device__ __forceinline__ int image_at(const VerifyGeom& g, int64_t t, int64_t& first_pixel) {
+    if (!g.offsets) {
+        const int64_t plane = int64_t(g.rows) * g.cols;
+        const int img = int(t / plane);
+        first_pixel = img * plane;
+        return img;
+    }
+    int lo = 0, hi = g.n - 1;  // last image with offsets[i] <= t
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (g.offsets[mid] <= t) lo = mid;
+        else hi = mid - 1;
+    }
+    first_pixel = g.offsets[lo];
+    return lo;
+}
+
+struct Fault {
+    int image, x, y, term, delta;  // image < 0: none
+};
+
+__device__ __forceinline__ void verify_pixel(const uint8_t* b, int rows, int cols, int pitch, int x,
+                                             int y, bool faulty, const Fault& f, int (&naive)[8],
+                                             int (&accel)[8]) {
+    constexpr int rdx[8] = {-1, -1, -1, 0, 1, 1, 1, 0}, rdy[8] = {-1, 0, 1, 1, 1, 0, -1, -1};
+    int ring[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        ring[j] = __ldg(b + int64_t(min(max(x + rdx[j], 0), rows - 1)) * pitch + min(max(y + rdy[j], 0), cols - 1));
+    naive8(ring, naive);
+    identity8(ring, accel);
+    if (faulty) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if ((c_term_users[f.term] >> i) & 1) accel[i] += f.delta;
+    }
+}
+
+// first[img] = min over mismatches of (x << 32 | y << 8 | direction).
+__global__ void __launch_bounds__(256) verify_kernel(VerifyGeom g, int64_t total, Fault f,
+                                                     unsigned long long* first,
+                                                     unsigned long long* mismatches) {
+    unsigned long long local = 0;
+    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total;
+         t += int64_t(gridDim.x) * blockDim.x) {
+        int64_t p0;
+        const int img = image_at(g, t, p0);
+        const uint8_t* b;
+        int rows, cols, pitch;
+        image_of(g, img, b, rows, cols, pitch);
+        const int64_t rem = t - p0;
+        const int x = int(rem / cols), y = int(rem - int64_t(x) * cols);
+        int naive[8], accel[8];
+        verify_pixel(b, rows, cols, pitch, x, y, img == f.image && x == f.x && y == f.y, f, naive, accel);
+        int dir = -1, cnt = 0;
+#pragma unroll
+        for (int i = 7; i >= 0; --i)
+            if (naive[i] != accel[i]) dir = i, ++cnt;
+        if (cnt) {
+            local += unsigned(cnt);
+            atomicMin(first + img,
+                      (static_cast<unsigned long long>(x) << 32) | (static_cast<unsigned long long>(y) << 8) |
+                          static_cast<unsigned long long>(dir));
+        }
+    }
+    if (local) atomicAdd(mismatches, local);
+}
+
+// Uniform batches: the same sweep over shared-memory tiles (all loads of a
+// tile in flight at once, rows re-used from registers).
+__global__ void __launch_bounds__(kFieldCols) verify_tiled_kernel(const uint8_t* __restrict__ px,
+                                                                  int64_t img_stride, int pitch, int rows,
+                                                                  int cols, int n_images, Fault f,
+                                                                  unsigned long long* first,
+                                                                  unsigned long long* mismatches) {
+    __shared__ uint8_t tile[kFieldRows + 2][kFieldPitch];
+    unsigned long long local = 0;
+    for_each_tile(px, img_stride, pitch, rows, cols, n_images, tile, [&](int img, int x0, int y, int h) {
+        slide(tile, h, [&](int r, const int (&ring)[8]) {
+            int naive[8], accel[8];
+            naive8(ring, naive);
+            identity8(ring, accel);
+            const int x = x0 + r;
+            if (img == f.image && x == f.x && y == f.y) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    if ((c_term_users[f.term] >> i) & 1) accel[i] += f.delta;
+            }
+            int dir = -1, cnt = 0;
+#pragma unroll
+            for (int i = 7; i >= 0; --i)
+                if (naive[i] != accel[i]) dir = i, ++cnt;
+            if (cnt) {
+                local += unsigned(cnt);
+                atomicMin(first + img, (static_cast<unsigned long long>(x) << 32) |
+                                           (static_cast<unsigned long long>(y) << 8) |
+                                           static_cast<unsigned long long>(dir));
+            }
+        });
+    });
+    if (local) atomicAdd(mismatches, local);
+}
+
+// Values of the reported mismatch (one thread; deterministic).
+__global__ void verify_values_kernel(VerifyGeom g, Fault f, int img, int x, int y, int dir, int* out2) {
+    const uint8_t* b;
+    int rows, cols, pitch;
+    image_of(g, img, b, rows, cols, pitch);
+    int naive[8], accel[8];
+    verify_pixel(b, rows, cols, pitch, x, y, img == f.image && x == f.x && y == f.y, f, naive, accel);
+    out2[0] = naive[dir];
+    out2[1] = accel[dir];
+}
+
+static int sm_count() {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : 148;
+}
+
+static aldp_status field_launch(const uint8_t* d_px, int64_t img_stride, int rows, int cols, int pitch,
+                                int n, int path, void* d_out, bool wide, cudaStream_t st) {
+    if (rows < 3 || cols < 3)
+        return set_error(ALDP_EINVAL, "descriptor extraction needs at least a 3x3 image, got " +
+                                          std::to_string(rows) + "x" + std::to_string(cols));
+    if (n < 0 || pitch < cols || (n > 0 && (!d_px || !d_out)) || (n > 1 && img_stride < int64_t(pitch) * rows))
+        return set_error(ALDP_EINVAL, "bad response-field arguments");
+    if (path != ALDP_PATH_NAIVE && path != ALDP_PATH_ACCELERATED)
+        return set_error(ALDP_EINVAL, "path must be ALDP_PATH_NAIVE or ALDP_PATH_ACCELERATED");
+    if (reinterpret_cast<uintptr_t>(d_out) % 16)
+        return set_error(ALDP_EINVAL, "response field output must be 16-byte aligned");
+    if (n == 0) return ALDP_OK;
+    const bool bulk = pitch % 16 == 0 && img_stride % 16 == 0 && reinterpret_cast<uintptr_t>(d_px) % 16 == 0 &&
+                      !std::getenv("ALDP_FIELD_NOBULK");
+    const bool naive = path == ALDP_PATH_NAIVE;
+    if (bulk) {
+        const int wchunk = std::min(cols, kRowChunk);
+        const int threads = ((wchunk + kRowCols - 1) / kRowCols + 31) / 32 * 32;
+        const int stride = (wchunk + 32 + 15) / 16 * 16;
+        const size_t smem = size_t(2) * (kRowBand + 2) * stride;
+        const int64_t tiles = int64_t(n) * ((rows + kRowBand - 1) / kRowBand) * ((cols + kRowChunk - 1) / kRowChunk);
+        auto go = [&](auto kernel, auto* o) {
+            int per_sm = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+            const int grid =
+                int(std::max<int64_t>(1, std::min<int64_t>(tiles, int64_t(sm_count()) * std::max(per_sm, 1))));
+            kernel<<<grid, threads, smem, st>>>(d_px, img_stride, pitch, rows, cols, n, stride, o);
+        };
+        if (wide) {
+            auto* o = static_cast<int32_t*>(d_out);
+            naive ? go(response_field_row_kernel<true, int32_t>, o) : go(response_field_row_kernel<false, int32_t>, o);
+        } else {
+            auto* o = static_cast<int16_t*>(d_out);
+            naive ? go(response_field_row_kernel<true, int16_t>, o) : go(response_field_row_kernel<false, int16_t>, o);
+        }
+    } else {
+        const int64_t tiles =
+            int64_t(n) * ((rows + kFieldRows - 1) / kFieldRows) * ((cols + kFieldCols - 1) / kFieldCols);
+        auto go = [&](auto kernel, auto* o) {
+            int per_sm = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kFieldCols, 0);
+            const int grid =
+                int(std::max<int64_t>(1, std::min<int64_t>(tiles, int64_t(sm_count()) * std::max(per_sm, 1))));
+            kernel<<<grid, kFieldCols, 0, st>>>(d_px, img_stride, pitch, rows, cols, n, o);
+        };
+        if (wide) {
+            auto* o = static_cast<int32_t*>(d_out);
+            naive ? go(response_field_kernel<true, int32_t>, o) : go(response_field_kernel<false, int32_t>, o);
+        } else {
+            auto* o = static_cast<int16_t*>(d_out);
+            naive ? go(response_field_kernel<true, int16_t>, o) : go(response_field_kernel<false, int16_t>, o);
+        }
+    }
+    FIELD_CUDA_TRY(cudaGetLastError());
+    return ALDP_OK;
+}
+
+// Runs the sweep; first_host[n] receives each image's first-mismatch key
+// (~0 when clean) and *count the total number of mismatching directions.
+static aldp_status verify_run(const VerifyGeom& g, int64_t total, const Fault& f, cudaStream_t st,
+                              std::vector<unsigned long long>& first_host, unsigned long long* count) {
+    first_host.assign(size_t(g.n), ~0ull);
+    *count = 0;
+    if (g.n == 0) return ALDP_OK;
+    unsigned long long* d = nullptr;
+    FIELD_CUDA_TRY(cudaMallocAsync(&d, sizeof(unsigned long long) * (size_t(g.n) + 1), st));
+    cudaError_t e = cudaMemsetAsync(d, 0xFF, sizeof(unsigned long long) * size_t(g.n), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(d + g.n, 0, sizeof(unsigned long long), st);
+    const int grid = int(std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, int64_t(sm_count()) * 16)));
+    if (e == cudaSuccess && total > 0) {
+        if (g.offsets) {
+            verify_kernel<<<grid, 256, 0, st>>>(g, total, f, d, d + g.n);
+        } else {
+            const int64_t tiles = int64_t(g.n) * ((g.rows + kFieldRows - 1) / kFieldRows) *
+                                  ((g.cols + kFieldCols - 1) / kFieldCols);
+            const int tgrid = int(std::max<int64_t>(1, std::min<int64_t>(tiles, int64_t(sm_count()) * 16)));
+            verify_tiled_kernel<<<tgrid, kFieldCols, 0, st>>>(g.px, g.img_stride, g.pitch, g.rows, g.cols, g.n,
+                                                              f, d, d + g.n);
+        }
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(first_host.data(), d, sizeof(unsigned long long) * size_t(g.n),
+                            cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(count, d + g.n, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(d, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    FIELD_CUDA_TRY(e);
+    return ALDP_OK;
+}
+
+static aldp_status mismatch_values(const VerifyGeom& g, const Fault& f, int img, aldp_verify_result* r,
+                                   cudaStream_t st) {
+    int* d = nullptr;
+    FIELD_CUDA_TRY(cudaMallocAsync(&d, sizeof(int) * 2, st));
+    verify_values_kernel<<<1, 1, 0, st>>>(g, f, img, r->x, r->y, r->direction, d);
+    int h[2] = {0, 0};
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(d, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    FIELD_CUDA_TRY(e);
+    r->naive_value = h[0];
+    r->accelerated_value = h[1];
+    return ALDP_OK;
+}
+
+// The reference's result bookkeeping (verify.cpp:63-111): images split into
+// `threads` ascending chunks of ceil(n/threads); each chunk stops after its
+// first mismatching image (counting that image's pixels up to and including
+// the mismatching one); the lowest chunk with a mismatch supplies it.
+// Returns the local index of the reported image (-1 when clean).
+static int assemble(const std::vector<unsigned long long>& first, const std::vector<int64_t>& pixels,
+                    const std::vector<int>& cols, int threads, int index_base, aldp_verify_result* r) {
+    const int n = int(first.size());
+    threads = std::clamp(threads, 1, std::max(n, 1));
+    const int chunk = n == 0 ? 0 : (n + threads - 1) / threads;
+    *r = aldp_verify_result{};
+    int found = -1;
+    for (int t = 0; t < threads; ++t) {
+        const int lo = t * chunk, hi = std::min(n, lo + chunk);
+        for (int i = lo; i < hi; ++i) {
+            r->images_checked += 1;
+            if (first[i] == ~0ull) {
+                r->pixels_checked += uint64_t(pixels[i]);
+                continue;
+            }
+            const int x = int(first[i] >> 32), y = int((first[i] >> 8) & 0xFFFFFF), dir = int(first[i] & 0xFF);
+            r->pixels_checked += uint64_t(int64_t(x) * cols[i] + y + 1);
+            if (found < 0) {
+                found = i;
+                r->has_mismatch = 1;
+                r->image_index = index_base + i, r->x = x, r->y = y, r->direction = dir;
+            }
+            break;
+        }
+    }
+    return found;
+}
+
+static Fault to_fault(const aldp_fault* f, int index_base, int n) {
+    if (!f) return Fault{-1, -1, -1, 0, 0};
+    const int img = f->image_index - index_base;
+    if (img < 0 || img >= n) return Fault{-1, -1, -1, 0, 0};
+    return Fault{img, f->x, f->y, f->term_index, f->delta};
+}
+
+static aldp_status check_fault(const aldp_fault* f) {
+    if (f && (f->term_index < 0 || f->term_index > 14))
+        return set_error(ALDP_ERANGE, "fault term_index must be in [0, 15) (ColumnTerms::a)");
+    return ALDP_OK;
+}
+
+static aldp_status finish(const VerifyGeom& g, const Fault& f, const std::vector<unsigned long long>& first,
+                          unsigned long long count, const std::vector<int64_t>& pixels,
+                          const std::vector<int>& cols, int threads, int index_base,
+                          aldp_verify_result* result, cudaStream_t st) {
+    const int img = assemble(first, pixels, cols, threads, index_base, result);
+    result->mismatches = count;
+    if (img < 0) return ALDP_OK;
+    return mismatch_values(g, f, img, result, st);
+}
+
+}  // namespace aldp_b200
+
+using namespace aldp_b200;
+
+extern "C" {
+
+aldp_status aldp_response_field_batch(const uint8_t* d_pixels, int64_t img_stride, int rows, int cols,
+                                      int pitch, int n_images, int path, int16_t* d_out, void* stream) {
+    return field_launch(d_pixels, img_stride, rows, cols, pitch, n_images, path, d_out, false,
+                        static_cast<cudaStream_t>(stream));
+}
+
+aldp_status aldp_response_field_batch32(const uint8_t* d_pixels, int64_t img_stride, int rows, int cols,
+                                        int pitch, int n_images, int path, int32_t* d_out, void* stream) {
+    return field_launch(d_pixels, img_stride, rows, cols, pitch, n_images, path, d_out, true,
+                        static_cast<cudaStream_t>(stream));
+}
+
+aldp_status aldp_response_field(const uint8_t* pixels, int rows, int cols, int path, int32_t* out) {
+    if (rows < 3 || cols < 3)
+        return set_error(ALDP_EINVAL, "descriptor extraction needs at least a 3x3 image, got " +
+                                          std::to_string(rows) + "x" + std::to_string(cols));
+    if (!pixels || !out) return set_error(ALDP_EINVAL, "null buffer");
+    if (path != ALDP_PATH_NAIVE && path != ALDP_PATH_ACCELERATED)
+        return set_error(ALDP_EINVAL, "path must be ALDP_PATH_NAIVE or ALDP_PATH_ACCELERATED");
+    cudaStream_t st = cudaStreamPerThread;
+    const size_t plane = size_t(rows) * cols;
+    uint8_t* d_px = nullptr;
+    int32_t* d_out = nullptr;
+    FIELD_CUDA_TRY(cudaMallocAsync(&d_px, plane, st));
+    cudaError_t e = cudaMallocAsync(&d_out, plane * 8 * sizeof(int32_t), st);
+    if (e != cudaSuccess) {
+        cudaFreeAsync(d_px, st);
+        FIELD_CUDA_TRY(e);
+    }
+    e = cudaMemcpyAsync(d_px, pixels, plane, cudaMemcpyHostToDevice, st);
+    aldp_status s = ALDP_ECUDA;
+    if (e == cudaSuccess) s = field_launch(d_px, int64_t(plane), rows, cols, cols, 1, path, d_out, true, st);
+    if (s == ALDP_OK) e = cudaMemcpyAsync(out, d_out, plane * 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(d_px, st);
+    cudaFreeAsync(d_out, st);
+    const cudaError_t e2 = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = e2;
+    FIELD_CUDA_TRY(e);
+    return s;
+}
+
+aldp_status aldp_verify_batch(const uint8_t* d_pixels, int64_t img_stride, int rows, int cols, int pitch,
+                              int n_images, const aldp_fault* fault, int threads,
+                              aldp_verify_result* result, void* stream) {
+    if (!result) return set_error(ALDP_EINVAL, "null result");
+    if (rows < 3 || cols < 3 || n_images < 0 || pitch < cols || (n_images > 0 && !d_pixels) ||
+        (n_images > 1 && img_stride < int64_t(pitch) * rows))
+        return set_error(ALDP_EINVAL, "bad verify arguments");
+    if (rows >= (1 << 24) || cols >= (1 << 24)) return set_error(ALDP_EINVAL, "image side too large");
+    aldp_status s = check_fault(fault);
+    if (s != ALDP_OK) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const VerifyGeom g{d_pixels, img_stride, pitch, rows, cols, n_images, nullptr, nullptr};
+    const Fault f = to_fault(fault, 0, n_images);
+    std::vector<unsigned long long> first;
+    unsigned long long count = 0;
+    s = verify_run(g, int64_t(rows) * cols * n_images, f, st, first, &count);
+    if (s != ALDP_OK) return s;
+    return finish(g, f, first, count, std::vector<int64_t>(size_t(n_images), int64_t(rows) * cols),
+                  std::vector<int>(size_t(n_images), cols), threads, 0, result, st);
+}
+
+aldp_status aldp_verify_image(const uint8_t* pixels, int rows, int cols, const aldp_fault* fault,
+                              int image_index, aldp_verify_result* result) {
+    if (!result || !pixels) return set_error(ALDP_EINVAL, "null buffer");
+    if (rows < 3 || cols < 3)
+        return set_error(ALDP_EINVAL, "descriptor extraction needs at least a 3x3 image, got " +
+                                          std::to_string(rows) + "x" + std::to_string(cols));
+    aldp_status s = check_fault(fault);
+    if (s != ALDP_OK) return s;
+    cudaStream_t st = cudaStreamPerThread;
+    const size_t plane = size_t(rows) * cols;
+    uint8_t* d_px = nullptr;
+    FIELD_CUDA_TRY(cudaMallocAsync(&d_px, plane, st));
+    cudaError_t e = cudaMemcpyAsync(d_px, pixels, plane, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) {
+        cudaFreeAsync(d_px, st);
+        FIELD_CUDA_TRY(e);
+    }
+    const VerifyGeom g{d_px, int64_t(plane), cols, rows, cols, 1, nullptr, nullptr};
+    const Fault f = to_fault(fault, image_index, 1);
+    std::vector<unsigned long long> first;
+    unsigned long long count = 0;
+    s = verify_run(g, int64_t(plane), f, st, first, &count);
+    if (s == ALDP_OK) s = finish(g, f, first, count, {int64_t(plane)}, {cols}, 1, image_index, result, st);
+    cudaFreeAsync(d_px, st);
+    cudaStreamSynchronize(st);
+    return s;
+}
+
+aldp_status aldp_verify_equivalence(int images, uint32_t seed, const aldp_fault* fault, int threads,
+                                    aldp_verify_result* result) {
+    if (!result) return set_error(ALDP_EINVAL, "null result");
+    aldp_status s = check_fault(fault);
+    if (s != ALDP_OK) return s;
+    images = std::max(images, 1);  // verify.hpp: images < 1 is clamped to 1
+    // corpus_specs (verify.cpp:22-33): sizes and per-image seeds from one mt19937
+    std::mt19937 rng(seed);
+    std::vector<int32_t> dims(size_t(images) * 2);
+    std::vector<uint32_t> seeds(static_cast<size_t>(images));
+    std::vector<int64_t> offsets(static_cast<size_t>(images) + 1, 0), pixels(static_cast<size_t>(images));
+    std::vector<int> cols(static_cast<size_t>(images));
+    for (int i = 0; i < images; ++i) {
+        dims[2 * i] = 3 + int32_t(rng() % 62);
+        dims[2 * i + 1] = 3 + int32_t(rng() % 62);
+        seeds[i] = rng();
+        cols[i] = dims[2 * i + 1];
+        pixels[i] = int64_t(dims[2 * i]) * dims[2 * i + 1];
+        offsets[i + 1] = offsets[i] + pixels[i];
+    }
+    // make_random (image.cpp:75-83): each image's own mt19937, low byte per
+    // pixel in raster order -- a sequential generator, run on host threads
+    std::vector<uint8_t> host(static_cast<size_t>(offsets[images]));
+    const int workers = int(std::clamp<unsigned>(std::thread::hardware_concurrency(), 1u, 32u));
+    {
+        std::vector<std::thread> pool;
+        for (int w = 0; w < workers; ++w)
+            pool.emplace_back([&, w] {
+                for (int i = w; i < images; i += workers) {
+                    std::mt19937 gen(seeds[i]);
+                    uint8_t* p = host.data() + offsets[i];
+                    for (int64_t j = 0; j < pixels[i]; ++j) p[j] = static_cast<uint8_t>(gen() & 0xFFu);
+                }
+            });
+        for (auto& t : pool) t.join();
+    }
+    cudaStream_t st = cudaStreamPerThread;
+    uint8_t* d_px = nullptr;
+    int64_t* d_off = nullptr;
+    int32_t* d_dims = nullptr;
+    cudaError_t e = cudaMallocAsync(&d_px, std::max<size_t>(host.size(), 1), st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&d_off, sizeof(int64_t) * offsets.size(), st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&d_dims, sizeof(int32_t) * dims.size(), st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_px, host.data(), host.size(), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(d_off, offsets.data(), sizeof(int64_t) * offsets.size(), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(d_dims, dims.data(), sizeof(int32_t) * dims.size(), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) {
+        const VerifyGeom g{d_px, 0, 0, 0, 0, images, d_off, d_dims};
+        const Fault f = to_fault(fault, 0, images);
+        std::vector<unsigned long long> first;
+        unsigned long long count = 0;
+        s = verify_run(g, offsets[images], f, st, first, &count);
+        if (s == ALDP_OK) s = finish(g, f, first, count, pixels, cols, threads, 0, result, st);
+    }
+    if (d_px) cudaFreeAsync(d_px, st);
+    if (d_off) cudaFreeAsync(d_off, st);
+    if (d_dims) cudaFreeAsync(d_dims, st);
+    cudaStreamSynchronize(st);
+    FIELD_CUDA_TRY(e);
+    return s;
+}
+
+}  // extern "C"

@@ -23,3 +23,10 @@ def golden_fixtures():
 def ref_vectors():
     import numpy as np
     return dict(np.load(os.path.join(GOLDEN, "ref_vectors.npz")))
+
+
+@pytest.fixture(scope="session")
+def verify_vectors():
+    import json
+    with open(os.path.join(GOLDEN, "verify_vectors.json")) as f:
+        return json.load(f)

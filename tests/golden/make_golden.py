@@ -18,6 +18,10 @@ Two sources, both the reference itself:
        * LBP code maps and lbp_histogram (aldp::lbp_code / lbp_histogram);
        * the config-1 image: make_random(490, 640, 42), its code map digest
          and whole-image histogram.
+  3. verify_vectors.json: aldp::verify_equivalence / verify_image results
+     (images/pixels checked, first mismatch) of the reference library for a
+     grid of seeds, faults and thread counts, and aldp::response_field of two
+     seeded images (naive and accelerated paths).
 """
 import hashlib
 import json
@@ -71,8 +75,44 @@ def ref_code_maps(img):
     return np.stack(maps)
 
 
+VERIFY_CASES = [
+    # (images, seed, fault (image, x, y, term, delta) or None, threads)
+    (1, 0, None, 1), (40, 7, None, 1), (40, 7, None, 4), (0, 3, None, 1),
+    (30, 9, (3, 2, 1, 0, 1), 1), (30, 9, (3, 2, 1, 11, -5), 3), (30, 9, (17, 1, 1, 14, 3), 8),
+    (30, 9, (10, 100, 1, 2, 1), 2), (30, 9, (0, 0, 0, 8, 0), 1), (30, 9, (29, 2, 2, 5, 7), 5),
+    (12, 1234567, (4, 0, 0, 3, -1), 1), (12, 1234567, (4, 0, 0, 3, -1), 12),
+    (64, 99, (63, 1, 2, 13, 100), 7), (64, 99, (5, 2, 2, 6, 1), 7),
+] + [(25, 2024, (7, 1, 1, t, 2), 1) for t in range(15)]
+
+
+def write_verify_vectors():
+    cases = []
+    for images, seed, fault, threads in VERIFY_CASES:
+        ic, pc, mm = oracle.ref_verify_equivalence(images, seed, fault, threads)
+        cases.append({"images": images, "seed": seed, "fault": fault, "threads": threads,
+                      "images_checked": ic, "pixels_checked": pc, "mismatch": mm})
+    img_cases = []
+    for i, (r, c) in enumerate([(3, 3), (9, 14), (33, 20)]):
+        img = oracle.ref_make_random(r, c, 500 + i)
+        for fault in (None, (0, r // 2, c // 2, 4, 1), (1, 0, 0, 4, 1), (0, r - 1, c - 1, 12, -9)):
+            ic, pc, mm = oracle.ref_verify_image(img, fault, 0)
+            img_cases.append({"rows": r, "cols": c, "seed": 500 + i, "fault": fault,
+                              "images_checked": ic, "pixels_checked": pc, "mismatch": mm})
+    fields = []
+    for r, c, seed in ((5, 7, 61), (34, 41, 62)):
+        img = oracle.ref_make_random(r, c, seed)
+        naive, accel = oracle.ref_response_field(img, 0), oracle.ref_response_field(img, 1)
+        assert np.array_equal(naive, accel)
+        fields.append({"rows": r, "cols": c, "seed": seed, "field": naive.ravel().tolist()})
+    with open(os.path.join(HERE, "verify_vectors.json"), "w") as f:
+        json.dump({"source": "reference verify_equivalence / verify_image / response_field via oracle/_ref",
+                   "equivalence": cases, "image": img_cases, "response_field": fields}, f)
+        f.write("\n")
+
+
 def main():
     convert_reference_fixtures()
+    write_verify_vectors()
     rng = np.random.default_rng(1810)
     vec = {}
     sizes = [(3, 3), (3, 7), (5, 4), (16, 16), (17, 31), (40, 64), (64, 130)]

@@ -51,7 +51,8 @@ def test_cpp_api_symbols_exported():
     out = subprocess.run(["nm", "-DC", aldp.LIB_PATH], capture_output=True, text=True).stdout
     for sym in ("aldp::ldp_histogram(", "aldp::windowed_features(", "aldp::ldp_code_map(",
                 "aldp::ldp_code(", "aldp::ldp_bin_index(", "aldp::make_grid(", "aldp::lbp_histogram(",
-                "aldp::lbp_code("):
+                "aldp::lbp_code(", "aldp::response_field(", "aldp::verify_equivalence(",
+                "aldp::verify_image("):
         assert sym in out, sym
 
 

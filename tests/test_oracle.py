@@ -175,3 +175,55 @@ def test_errors():
         oracle.ref_windowed(np.zeros((10, 10), np.uint8), 11)     # window > image
     with pytest.raises(IndexError):
         oracle.ref_responses(np.zeros((5, 5), np.uint8), 5, 0)    # out_of_range
+
+# ------------------------------------- response field / equivalence sweep
+
+def _mm(m):
+    return None if m is None else tuple(m)
+
+
+def test_port_response_field_matches_reference(golden_fixtures, verify_vectors):
+    """kirsch.cpp:193-208 on the reference's fixtures and reference outputs."""
+    for fx in golden_fixtures:
+        img = np.array(fx["pixels"], np.uint8).reshape(fx["rows"], fx["cols"])
+        assert oracle.response_field(img).tolist() == fx["responses"], fx["name"]
+    for f in verify_vectors["response_field"]:
+        img = oracle.make_random(f["rows"], f["cols"], f["seed"])
+        assert oracle.response_field(img).ravel().tolist() == f["field"]
+
+
+def test_port_column_terms_reconstruct_naive():
+    """kirsch.cpp:86-157: three column terms per response == the naive sum."""
+    rng = np.random.default_rng(21)
+    for _ in range(5):
+        r, c = rng.integers(3, 12, size=2)
+        img = rng.integers(0, 256, size=(r, c), dtype=np.uint8)
+        for x in range(r):
+            for y in range(c):
+                assert np.array_equal(oracle.responses_terms(oracle.column_terms(img, x, y)),
+                                      oracle.responses(img, x, y))
+
+
+def test_port_verify_matches_reference_vectors(verify_vectors):
+    """verify.cpp:37-111: counts, first mismatch and thread bookkeeping."""
+    for c in verify_vectors["equivalence"]:
+        got = oracle.verify_equivalence(c["images"], c["seed"], c["fault"], c["threads"])
+        assert got == (c["images_checked"], c["pixels_checked"], _mm(c["mismatch"])), c
+    for c in verify_vectors["image"]:
+        img = oracle.make_random(c["rows"], c["cols"], c["seed"])
+        got = oracle.verify_image(img, c["fault"], 0)
+        assert got == (c["images_checked"], c["pixels_checked"], _mm(c["mismatch"])), c
+    assert any(c["mismatch"] for c in verify_vectors["equivalence"])
+    assert any(c["mismatch"] is None for c in verify_vectors["equivalence"])
+
+
+@pytest.mark.skipif(not oracle.have_ref(), reason="reference library not built")
+def test_port_verify_matches_reference_library():
+    rng = np.random.default_rng(8)
+    for _ in range(20):
+        images, seed, threads = int(rng.integers(1, 20)), int(rng.integers(0, 2**32)), int(rng.integers(1, 9))
+        fault = None if rng.random() < 0.3 else (int(rng.integers(0, images)), int(rng.integers(0, 5)),
+                                                  int(rng.integers(0, 5)), int(rng.integers(0, 15)),
+                                                  int(rng.integers(-3, 4)))
+        assert oracle.verify_equivalence(images, seed, fault, threads) == \
+            oracle.ref_verify_equivalence(images, seed, fault, threads)
