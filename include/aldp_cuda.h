@@ -38,7 +38,8 @@ typedef enum {
     ALDP_EINVAL = 1, /* maps to std::invalid_argument in the C++ layer */
     ALDP_ERANGE = 2, /* maps to std::out_of_range */
     ALDP_ECUDA = 3,  /* CUDA runtime failure -> std::runtime_error */
-    ALDP_ENOMEM = 4  /* device/host allocation failure -> std::runtime_error */
+    ALDP_ENOMEM = 4, /* device/host allocation failure -> std::runtime_error */
+    ALDP_EIO = 5     /* file I/O or PGM format error -> std::runtime_error (pgm.hpp:15-17) */
 } aldp_status;
 
 /* Response path selector, mirroring aldp::ResponsePath (kirsch.hpp:88) and
@@ -190,6 +191,45 @@ aldp_status aldp_verify_image(const uint8_t* pixels, int rows, int cols, const a
 aldp_status aldp_verify_batch(const uint8_t* d_pixels, int64_t img_stride, int rows, int cols, int pitch,
                               int n_images, const aldp_fault* fault, int threads,
                               aldp_verify_result* result, void* stream);
+
+/* ---- on-disk input and report formats ---- */
+
+/* aldp::load_pgm (include/aldp/pgm.hpp:15-18, src/pgm.cpp:59-125): P5/P2,
+ * maxval <= 255, '#' comments. Writes *rows / *cols (height / width); with
+ * out == NULL only the header is read (size query). Format and I/O errors ->
+ * ALDP_EIO with the reference's "<path>: <what>" message; cap too small ->
+ * ALDP_EINVAL. */
+aldp_status aldp_load_pgm(const char* path, uint8_t* out, size_t cap, int* rows, int* cols);
+/* aldp::save_pgm (pgm.hpp:20-23): maxval 255, ascii != 0 -> P2. */
+aldp_status aldp_save_pgm(const char* path, const uint8_t* pixels, int rows, int cols, int ascii);
+/* n equal-size PGM files decoded on `threads` host threads into out
+ * [n][rows][cols] (e.g. pinned, then aldp_ldp_batch_host). A file of another
+ * size -> ALDP_EINVAL. */
+aldp_status aldp_load_pgm_batch(const char* const* paths, int n, int rows, int cols, uint8_t* out, int threads);
+
+/* The CLI's `extract` (tools/aldp_main.cpp:59-96) as one call: CSV header
+ * "identifier,descriptor,bin_0..", one row per file (window == 0) or per
+ * window "<path>#w<i>" (window >= 3), descriptor "lbp" | "ldp" | "aldp"
+ * (case-insensitive), out_path NULL or "" -> stdout. Files are decoded by a
+ * thread pool (threads < 1: all cores) one group ahead of the B200, which
+ * extracts runs of equal-size images from pinned staging. Rows already
+ * written stay written when a later file fails (as the reference streams). */
+aldp_status aldp_extract_files(const char* const* paths, int n, const char* descriptor, int window,
+                               const char* out_path, int threads);
+
+/* aldp::measured_ops (bench.hpp:42-44): per-pixel (mults, adds) of the
+ * reference's arithmetic model; descriptor = ALDP_PATH_NAIVE (LDP),
+ * ALDP_PATH_ACCELERATED (ALDP) or ALDP_DESC_LBP. */
+aldp_status aldp_op_counts(int descriptor, int* mults, int* adds);
+
+/* The CLI's `bench` (aldp_main.cpp:128-165, bench.cpp:134-178): series
+ * "images" (side `size`, default 260, prefixes `counts`) or "window" (side
+ * default 300, `windows`), median of `repeats` (>= 3), all three descriptors
+ * or the one named, CSV in the reference's schema to out_path (NULL/"" ->
+ * stdout). Every timed extraction runs on the B200. */
+aldp_status aldp_bench_csv(const char* series, int size, const int* counts, int n_counts, const int* windows,
+                           int n_windows, int repeats, uint32_t seed, const char* descriptor,
+                           const char* out_path);
 
 /* Message for the last non-OK status returned on this host thread. */
 const char* aldp_last_error(void);

@@ -62,6 +62,10 @@ def _load_ref():
     L.ref_response_field.argtypes = [_P, _I, _I, _I, _P]
     L.ref_verify_equivalence.argtypes = [_I, _U32, _P, _I, _P, _P]
     L.ref_verify_image.argtypes = [_P, _I, _I, _P, _I, _P, _P]
+    L.ref_load_pgm.argtypes = [ctypes.c_char_p, _P, ctypes.c_size_t, _P, _P, _P, _I]
+    L.ref_save_pgm.argtypes = [ctypes.c_char_p, _P, _I, _I, _I]
+    L.ref_op_counts.argtypes = [_I, _P, _P]
+    L.ref_bench_csv.argtypes = [ctypes.c_char_p, _I, _P, _I, _P, _I, _I, _U32, _I, _P, ctypes.c_size_t]
     return L
 
 
@@ -310,3 +314,46 @@ def ref_verify_image(img, fault=None, image_index: int = 0):
                               mm.ctypes.data):
         raise RuntimeError("reference verify failed")
     return _verify_tuple(counts, mm)
+
+
+# ---- PGM I/O and op counts: the reference itself ----
+def ref_load_pgm(path):
+    """(pixels [rows, cols] uint8, None) or (None, runtime_error message)."""
+    rows, cols = ctypes.c_int(), ctypes.c_int()
+    err = ctypes.create_string_buffer(1024)
+    p = os.fsencode(path)
+    st = ref().ref_load_pgm(p, None, 0, ctypes.byref(rows), ctypes.byref(cols), err, 1024)
+    if st == 4:
+        return None, err.value.decode(errors="replace")
+    if st:
+        raise RuntimeError(f"reference load_pgm status {st}")
+    out = np.empty((rows.value, cols.value), np.uint8)
+    st = ref().ref_load_pgm(p, out.ctypes.data, out.size, ctypes.byref(rows), ctypes.byref(cols), err, 1024)
+    assert st == 0
+    return out, None
+
+
+def ref_save_pgm(path, img, ascii: bool = False):
+    a = _img(img)
+    if ref().ref_save_pgm(os.fsencode(path), a.ctypes.data, a.shape[0], a.shape[1], int(ascii)):
+        raise RuntimeError("reference save_pgm failed")
+
+
+def ref_op_counts(descriptor: int):
+    """descriptor 0 LDP, 1 ALDP, 2 LBP -> (mults, adds) per pixel."""
+    m, a = ctypes.c_int(), ctypes.c_int()
+    if ref().ref_op_counts(descriptor, ctypes.byref(m), ctypes.byref(a)):
+        raise RuntimeError("reference measured_ops failed")
+    return m.value, a.value
+
+
+def ref_bench_csv(series="images", size=0, counts=(1, 2, 4, 6, 8, 10), windows=(25, 50, 100), repeats=5,
+                  seed=42, descriptor=-1) -> str:
+    """The reference CLI's bench report (CPU), descriptor -1 = all three."""
+    c = (ctypes.c_int * max(len(counts), 1))(*counts)
+    w = (ctypes.c_int * max(len(windows), 1))(*windows)
+    buf = ctypes.create_string_buffer(1 << 16)
+    if ref().ref_bench_csv(series.encode(), size, c, len(counts), w, len(windows), repeats, seed, descriptor,
+                           buf, len(buf)):
+        raise RuntimeError("reference bench failed")
+    return buf.value.decode()

@@ -21,11 +21,17 @@
 //                        (src/descriptors.cpp:141-168), windowed_features(Lbp)
 //   ref_response_field   aldp::response_field             (src/kirsch.cpp:193-208)
 //   ref_verify_*         aldp::verify_equivalence / verify_image (src/verify.cpp:37-111)
+//   ref_load_pgm         aldp::load_pgm                   (src/pgm.cpp:59-125)
+//   ref_save_pgm         aldp::save_pgm                   (src/pgm.cpp:127-149)
+//   ref_op_counts        aldp::measured_ops               (src/bench.cpp:97-116)
 //   ref_batch            the above over a batch, std::thread sharded by image
 //                        (the reference functions are pure)
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <sstream>
+#include <string>
 #include <stdexcept>
 #include <thread>
 #include <vector>
@@ -34,6 +40,7 @@
 #include "aldp/descriptors.hpp"
 #include "aldp/image.hpp"
 #include "aldp/kirsch.hpp"
+#include "aldp/pgm.hpp"
 #include "aldp/verify.hpp"
 #include "aldp/windowing.hpp"
 
@@ -258,6 +265,88 @@ int ref_verify_image(const uint8_t* px, int rows, int cols, const int* fault5, i
                      uint64_t* counts2, int* mm7) {
     return guarded([&] {
         flatten(aldp::verify_image(wrap(px, rows, cols), fault_of(fault5), image_index), counts2, mm7);
+    });
+}
+
+// aldp::load_pgm: 0 ok (rows/cols/pixels), 4 std::runtime_error (message in
+// err), other codes as guarded(). out == NULL: dimensions only.
+int ref_load_pgm(const char* path, uint8_t* out, size_t cap, int* rows, int* cols, char* err, int err_len) {
+    try {
+        const aldp::GrayImage img = aldp::load_pgm(path);
+        *rows = img.rows(), *cols = img.cols();
+        if (out) {
+            if (cap < img.pixel_count()) return 1;
+            std::memcpy(out, img.pixels().data(), img.pixel_count());
+        }
+        return 0;
+    } catch (const std::runtime_error& e) {
+        if (err && err_len > 0) {
+            std::strncpy(err, e.what(), size_t(err_len) - 1);
+            err[err_len - 1] = 0;
+        }
+        return 4;
+    } catch (const std::invalid_argument&) {
+        return 1;
+    } catch (...) {
+        return 3;
+    }
+}
+
+int ref_save_pgm(const char* path, const uint8_t* px, int rows, int cols, int ascii) {
+    return guarded([&] {
+        aldp::save_pgm(path, wrap(px, rows, cols), ascii ? aldp::PgmFormat::Ascii : aldp::PgmFormat::Binary);
+    });
+}
+
+// descriptor: 0 LDP, 1 ALDP, 2 LBP
+int ref_op_counts(int descriptor, int* mults, int* adds) {
+    return guarded([&] {
+        const auto d = descriptor == 2 ? aldp::Descriptor::Lbp
+                                       : descriptor == 0 ? aldp::Descriptor::Ldp : aldp::Descriptor::Aldp;
+        const aldp::OpCountRow r = aldp::measured_ops(d);
+        *mults = r.multiplications;
+        *adds = r.additions;
+    });
+}
+
+// The reference CLI's `bench` body (tools/aldp_main.cpp:128-165) over the
+// reference library: run_time_series / run_window_series + write_csv into
+// `out` (NUL-terminated, truncated to cap).
+int ref_bench_csv(const char* series, int size, const int* counts, int n_counts, const int* windows,
+                  int n_windows, int repeats, uint32_t seed, int descriptor, char* out, size_t cap) {
+    return guarded([&] {
+        std::vector<aldp::Descriptor> ds = {aldp::Descriptor::Lbp, aldp::Descriptor::Ldp, aldp::Descriptor::Aldp};
+        if (descriptor >= 0)
+            ds = {descriptor == 2 ? aldp::Descriptor::Lbp
+                                  : descriptor == 0 ? aldp::Descriptor::Ldp : aldp::Descriptor::Aldp};
+        std::vector<aldp::BenchRecord> records;
+        if (std::string(series) == "images") {
+            const int side = size > 0 ? size : 260;
+            std::vector<int> cs(counts, counts + n_counts);
+            int corpus_size = 1;
+            for (int c : cs) corpus_size = std::max(corpus_size, c);
+            std::vector<aldp::GrayImage> corpus;
+            for (int i = 0; i < corpus_size; ++i)
+                corpus.push_back(aldp::make_random(side, side, seed + static_cast<uint32_t>(i)));
+            for (auto d : ds) {
+                const auto rows = aldp::run_time_series(corpus, d, repeats, cs);
+                records.insert(records.end(), rows.begin(), rows.end());
+            }
+        } else {
+            const int side = size > 0 ? size : 300;
+            const aldp::GrayImage img = aldp::make_random(side, side, seed);
+            std::vector<int> ws(windows, windows + n_windows);
+            for (auto d : ds) {
+                const auto rows = aldp::run_window_series(img, ws, d, repeats);
+                records.insert(records.end(), rows.begin(), rows.end());
+            }
+        }
+        std::ostringstream os;
+        aldp::write_csv(os, records);
+        const std::string s = os.str();
+        const size_t n = std::min(cap - 1, s.size());
+        std::memcpy(out, s.data(), n);
+        out[n] = 0;
     });
 }
 

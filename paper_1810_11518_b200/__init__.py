@@ -37,6 +37,8 @@ __all__ = [
     "ldp_batch", "ldp_batch_host", "gen_faces", "gen_ties", "version",
     "lbp_histogram", "lbp_code_map", "lbp_batch", "response_field", "response_field_batch",
     "FaultInjection", "Mismatch", "VerifyResult", "verify_equivalence", "verify_image", "verify_batch",
+    "PgmError", "load_pgm", "save_pgm", "load_pgm_batch", "extract_files", "op_counts", "bench_csv",
+    "CLI_PATH",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -70,7 +72,12 @@ class AldpError(RuntimeError):
     pass
 
 
-_STATUS_EXC = {1: ValueError, 2: IndexError, 3: AldpError, 4: MemoryError}
+class PgmError(AldpError):
+    """File I/O or PGM format error (the reference's std::runtime_error from
+    load_pgm / save_pgm, pgm.hpp:15-17)."""
+
+
+_STATUS_EXC = {1: ValueError, 2: IndexError, 3: AldpError, 4: MemoryError, 5: PgmError}
 
 
 class _Args(ctypes.Structure):
@@ -130,6 +137,13 @@ def _load() -> ctypes.CDLL:
         "aldp_verify_image": ([P, I, I, ctypes.POINTER(_Fault), I, ctypes.POINTER(_VerifyResult)], I),
         "aldp_verify_batch": ([P, I64, I, I, I, I, ctypes.POINTER(_Fault), I,
                                ctypes.POINTER(_VerifyResult), P], I),
+        "aldp_load_pgm": ([ctypes.c_char_p, P, ctypes.c_size_t, P, P], I),
+        "aldp_save_pgm": ([ctypes.c_char_p, P, I, I, I], I),
+        "aldp_load_pgm_batch": ([P, I, I, I, P, I], I),
+        "aldp_extract_files": ([P, I, ctypes.c_char_p, I, ctypes.c_char_p, I], I),
+        "aldp_op_counts": ([I, P, P], I),
+        "aldp_bench_csv": ([ctypes.c_char_p, I, P, I, P, I, I, ctypes.c_uint32, ctypes.c_char_p,
+                            ctypes.c_char_p], I),
     }
     for name, (argtypes, restype) in sig.items():
         fn = getattr(L, name)
@@ -487,3 +501,75 @@ def verify_batch(pixels, rows: int, cols: int, fault: Optional[FaultInjection] =
     _check(lib.aldp_verify_batch(pixels.data_ptr(), rows * pitch, rows, cols, pitch, n, _fault_arg(fault),
                                  int(threads), ctypes.byref(r), stream or None))
     return _result(r)
+
+
+# ------------------------------------------------------------ files and reports
+
+CLI_PATH = os.path.join(_HERE, "aldp_b200")  # the command-line front end (aldp_main.cpp)
+
+
+def load_pgm(path) -> np.ndarray:
+    """aldp::load_pgm (pgm.hpp:15-18): [rows, cols] uint8; PgmError on any
+    I/O or format problem, with the reference's "<path>: <what>" message."""
+    p = os.fsencode(path)
+    rows, cols = ctypes.c_int(), ctypes.c_int()
+    _check(lib.aldp_load_pgm(p, None, 0, ctypes.byref(rows), ctypes.byref(cols)))
+    out = np.empty((rows.value, cols.value), np.uint8)
+    _check(lib.aldp_load_pgm(p, out.ctypes.data, out.size, ctypes.byref(rows), ctypes.byref(cols)))
+    return out
+
+
+def save_pgm(path, img, ascii: bool = False) -> None:
+    """aldp::save_pgm (pgm.hpp:20-23): maxval 255, P5 (default) or P2."""
+    img = np.ascontiguousarray(np.asarray(img, dtype=np.uint8))
+    if img.ndim != 2:
+        raise ValueError("expected a 2-D uint8 image (rows x cols)")
+    _check(lib.aldp_save_pgm(os.fsencode(path), img.ctypes.data, img.shape[0], img.shape[1], int(ascii)))
+
+
+def _c_paths(paths):
+    enc = [os.fsencode(p) for p in paths]
+    arr = (ctypes.c_char_p * max(len(enc), 1))(*enc)
+    return arr, enc
+
+
+def load_pgm_batch(paths, rows: int, cols: int, out: Optional[np.ndarray] = None, threads: int = 0) -> np.ndarray:
+    """Equal-size PGM files decoded on host threads into [n, rows, cols]
+    (out may be pinned memory, e.g. a pinned torch tensor's numpy view)."""
+    n = len(paths)
+    if out is None:
+        out = np.empty((n, rows, cols), np.uint8)
+    if out.dtype != np.uint8 or not out.flags.c_contiguous or out.size < n * rows * cols:
+        raise ValueError("out must be a contiguous uint8 array of n*rows*cols")
+    arr, keep = _c_paths(paths)
+    _check(lib.aldp_load_pgm_batch(arr, n, rows, cols, out.ctypes.data, int(threads or os.cpu_count() or 1)))
+    return out
+
+
+def extract_files(paths, descriptor: str = "aldp", window: int = 0, out_path=None, threads: int = 0) -> None:
+    """The CLI's `extract` (aldp_main.cpp:59-96): CSV of per-file (or
+    per-window) histograms to out_path (None -> stdout)."""
+    arr, keep = _c_paths(paths)
+    _check(lib.aldp_extract_files(arr, len(paths), str(descriptor).encode(), int(window),
+                                  None if out_path is None else os.fsencode(out_path), int(threads)))
+
+
+def op_counts(descriptor) -> Tuple[int, int]:
+    """aldp::measured_ops (bench.hpp:42-44): (mults, adds) per pixel."""
+    if isinstance(descriptor, str):
+        descriptor = parse_descriptor(descriptor)
+    code = {Descriptor.Ldp: 0, Descriptor.Aldp: 1, Descriptor.Lbp: 2}[descriptor]
+    m, a = ctypes.c_int(), ctypes.c_int()
+    _check(lib.aldp_op_counts(code, ctypes.byref(m), ctypes.byref(a)))
+    return m.value, a.value
+
+
+def bench_csv(series: str = "images", size: int = 0, counts=(1, 2, 4, 6, 8, 10), windows=(25, 50, 100),
+              repeats: int = 5, seed: int = 42, descriptor: str = "", out_path=None) -> None:
+    """The CLI's `bench` (bench.cpp:134-178): the reference's CSV schema,
+    every timed extraction on the B200."""
+    c = (ctypes.c_int * max(len(counts), 1))(*counts)
+    w = (ctypes.c_int * max(len(windows), 1))(*windows)
+    _check(lib.aldp_bench_csv(series.encode(), int(size), c, len(counts), w, len(windows), int(repeats),
+                              int(seed) & 0xFFFFFFFF, descriptor.encode(),
+                              None if out_path is None else os.fsencode(out_path)))

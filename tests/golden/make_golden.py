@@ -82,7 +82,9 @@ VERIFY_CASES = [
     (30, 9, (10, 100, 1, 2, 1), 2), (30, 9, (0, 0, 0, 8, 0), 1), (30, 9, (29, 2, 2, 5, 7), 5),
     (12, 1234567, (4, 0, 0, 3, -1), 1), (12, 1234567, (4, 0, 0, 3, -1), 12),
     (64, 99, (63, 1, 2, 13, 100), 7), (64, 99, (5, 2, 2, 6, 1), 7),
-] + [(25, 2024, (7, 1, 1, t, 2), 1) for t in range(15)]
+] + [(25, 2024, (7, 1, 1, t, 2), 1) for t in range(15)] + [
+    (1000, 42, None, 1), (1000, 42, (0, 1, 1, 0, 1), 1),  # the CLI's `verify` defaults (aldp_main.cpp:97-126)
+]
 
 
 def write_verify_vectors():
