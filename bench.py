@@ -240,12 +240,19 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--kernel", default="auto", choices=["auto", "fast", "generic"])
+    ap.add_argument("--force-dist", action="store_true",
+                    help="initialise NCCL and run the histogram gather even at world size 1 (tests the path)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
 
     if args.impl == "reference":
         return run_reference(args, args.config)
+
+    # The JSON line is the only thing on stdout: libraries that print from C
+    # (NCCL's version banner at communicator init) go to stderr instead.
+    out_fd = os.dup(1)
+    os.dup2(2, 1)
 
     import numpy as np
     import torch
@@ -258,7 +265,8 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    use_dist = world > 1 or args.force_dist
+    if use_dist:
         dist.init_process_group("nccl", device_id=dev)
 
     n, rows, cols, k, cr, cc, blobs, gen, seed = CONFIGS[args.config]
@@ -286,7 +294,7 @@ def main():
         codes = torch.empty((mine, rows, pitch), dtype=torch.uint8, device=dev)
         hist = torch.empty((mine, cells, nb), dtype=torch.int32, device=dev)
         gathered = None
-        if world > 1:
+        if use_dist:
             # uint16 on the wire: a cell count is at most 81*91 = 7371 < 65536
             assert wire_dtype_ok((cr or rows) * (cc or cols))
             per = [shard_range(n, r, world)[1] - shard_range(n, r, world)[0] for r in range(world)]
@@ -299,7 +307,7 @@ def main():
     def step():
         aldp.ldp_batch(px, rows, cols, k=k, cell=(cr, cc), codes=codes, hist=hist,
                        kernel=args.kernel, stream=sp)
-        if world > 1:
+        if use_dist:
             with torch.cuda.stream(stream):
                 gather_histograms(hist, dist, rank, world, wire=wire, out=gathered)
 
@@ -311,7 +319,7 @@ def main():
     # ---- timed region: K steps, events on the launching stream ----
     sampler = ClockSampler(local) if True else None
     sampler.start()
-    if world > 1:
+    if use_dist:
         dist.barrier()
     torch.cuda.synchronize(dev)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
@@ -323,17 +331,17 @@ def main():
         aldp.ldp_batch(px, rows, cols, k=k, cell=(cr, cc), codes=codes, hist=hist,
                        kernel=args.kernel, stream=sp)
         ev[2 * i + 1].record(stream)
-        if world > 1:
+        if use_dist:
             with torch.cuda.stream(stream):
                 gather_histograms(hist, dist, rank, world, wire=wire, out=gathered)
     t_end.record(stream)
     torch.cuda.synchronize(dev)
-    if world > 1:
+    if use_dist:
         dist.barrier()
     clocks = sampler.stop()
     total_ms = t_start.elapsed_time(t_end)
     launch_ms = sum(ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(args.steps)) / args.steps
-    if world > 1:
+    if use_dist:
         t = torch.tensor([total_ms, launch_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms, launch_ms = float(t[0]), float(t[1])
@@ -373,7 +381,9 @@ def main():
     }
 
     # ---- end to end through the host C-ABI (pinned host buffers) ----
-    if not args.no_e2e and rank == 0 and world == 1:
+    # Every rank runs its own host batch through its own PCIe link at the
+    # same time; the value is all ranks' pixels over the slowest rank's time.
+    if not args.no_e2e:
         import ctypes
         e2n = min(args.e2e_images, mine)
         hp = torch.empty((e2n, rows, cols), dtype=torch.uint8).pin_memory()
@@ -392,16 +402,28 @@ def main():
 
         for _ in range(args.warmup):
             e2e_call()
+        if use_dist:
+            dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
             e2e_call()
         e2e_dt = (time.perf_counter() - t0) / args.steps
-        line["e2e"] = {"value": round(e2n * rows * cols / e2e_dt / 1e6, 1), "unit": "Mpixel/s",
+        if use_dist:
+            t = torch.tensor([e2e_dt], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_dt = float(t[0])
+        line["e2e"] = {"value": round(world * e2n * rows * cols / e2e_dt / 1e6, 1), "unit": "Mpixel/s",
                        "h2d_bytes_per_step": int(hp.numel()),
                        "d2h_bytes_per_step": int(hc.numel() + hh.numel() * 4),
-                       "images_per_step": e2n, "api": "aldp_ldp_batch_host (C-ABI, host buffers)"}
+                       "images_per_step": e2n * world, "ranks": world,
+                       "timing": "host wall clock per rank, max over ranks",
+                       "api": "aldp_ldp_batch_host (C-ABI, host buffers)"}
         ok = np.array_equal(hc.numpy(), codes[:e2n, :, :cols].cpu().numpy()) and \
             np.array_equal(hh.numpy(), hist[:e2n].cpu().numpy())
+        if use_dist:
+            t = torch.tensor([0 if ok else 1], device=dev, dtype=torch.int32)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ok = int(t[0]) == 0
         line["e2e"]["matches_device_path"] = bool(ok)
 
     # ---- CPU baseline (reference library on this box's host cores) ----
@@ -413,8 +435,9 @@ def main():
         line["cpu_baseline"] = cpu_baseline(host, k, cr if rows * cols < 1e8 else cr,
                                             cc if rows * cols < 1e8 else cc)
     if rank == 0:
-        print(json.dumps(line), flush=True)
-    if world > 1:
+        sys.stdout.flush()
+        os.write(out_fd, (json.dumps(line) + "\n").encode())
+    if use_dist:
         dist.destroy_process_group()
     return 0
 
