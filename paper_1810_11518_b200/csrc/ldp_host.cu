@@ -39,6 +39,7 @@ static aldp_status hfail(aldp_status s, const std::string& msg) { return set_err
 // (separate copy engines per direction; stream order protects buffer reuse).
 constexpr int kSlots = 3;
 constexpr size_t kChunkBytes = size_t(48) << 20;  // pixel bytes per chunk (~150 640x490 frames)
+constexpr size_t kSmallBytes = size_t(4) << 20;   // calls up to this many pixel bytes take the staged path
 
 struct Slot {
     cudaStream_t stream = nullptr;
@@ -57,12 +58,27 @@ struct Slot {
     }
 };
 
+// Pinned host staging for small calls (grow-only, per thread).
+struct PinnedBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
 struct HostCtx {
     int device = -1;
     Slot slot[kSlots];
+    PinnedBuf h_px, h_codes, h_hist;
     ~HostCtx() {
         // Process teardown: the CUDA context may already be gone; ignore errors.
         for (auto& s : slot) s.release();
+        h_px.release();
+        h_codes.release();
+        h_hist.release();
     }
 };
 static thread_local HostCtx t_ctx;
@@ -77,11 +93,22 @@ static aldp_status ensure(void** p, size_t* cap, size_t need) {
     return ALDP_OK;
 }
 
+static aldp_status ensure_pinned(PinnedBuf& b, size_t need) {
+    if (b.cap >= need) return ALDP_OK;
+    b.release();
+    HOST_CUDA_TRY(cudaHostAlloc(&b.p, need, cudaHostAllocDefault));
+    b.cap = need;
+    return ALDP_OK;
+}
+
 static aldp_status ctx_ready(HostCtx& c) {
     int dev = 0;
     HOST_CUDA_TRY(cudaGetDevice(&dev));
     if (c.device != dev) {  // a different device on this thread: drop the old buffers
         for (auto& s : c.slot) s.release();
+        c.h_px.release();
+        c.h_codes.release();
+        c.h_hist.release();
         for (auto& s : c.slot) HOST_CUDA_TRY(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
         c.device = dev;
     }
@@ -117,6 +144,60 @@ static aldp_status host_batch(const uint8_t* px, int n, int rows, int cols, int 
     const int chunk = int(std::max<size_t>(1, std::min<size_t>(size_t(n), kChunkBytes / img_bytes)));
     const int n_chunks = (n + chunk - 1) / chunk;
     const int used = std::min(n_chunks, kSlots);
+    // Small calls (the reference's one-image-per-call pattern): stage through
+    // pinned host buffers on one stream. The CPU does the pitch padding, so
+    // every transfer is a single 1D DMA instead of a pageable (2D) copy.
+    if (!user && img_bytes * size_t(n) <= kSmallBytes) {
+        Slot& sl = c.slot[0];
+        s = ensure(reinterpret_cast<void**>(&sl.d_px), &sl.px_cap, img_bytes * n);
+        if (s == ALDP_OK && codes) s = ensure(reinterpret_cast<void**>(&sl.d_codes), &sl.codes_cap, img_bytes * n);
+        if (s == ALDP_OK && hist32)
+            s = ensure(reinterpret_cast<void**>(&sl.d_hist), &sl.hist_cap, sizeof(uint32_t) * hist_per_img * n);
+        if (s == ALDP_OK) s = ensure_pinned(c.h_px, img_bytes * n);
+        if (s == ALDP_OK && codes) s = ensure_pinned(c.h_codes, img_bytes * n);
+        if (s == ALDP_OK && hist32) s = ensure_pinned(c.h_hist, sizeof(uint32_t) * hist_per_img * n);
+        if (s != ALDP_OK) return s;
+        uint8_t* hp = static_cast<uint8_t*>(c.h_px.p);
+        if (pitch == cols) {
+            std::memcpy(hp, px, plane * n);
+        } else {
+            for (size_t r = 0; r < size_t(rows) * n; ++r) std::memcpy(hp + r * pitch, px + r * cols, cols);
+        }
+        const cudaStream_t st = sl.stream;
+        HOST_CUDA_TRY(cudaMemcpyAsync(sl.d_px, hp, img_bytes * n, cudaMemcpyHostToDevice, st));
+        aldp_ldp_args a{};
+        a.d_pixels = sl.d_px;
+        a.img_stride = int64_t(img_bytes);
+        a.rows = rows;
+        a.cols = cols;
+        a.pitch = pitch;
+        a.n_images = n;
+        a.k = k;
+        a.cell_rows = cell_rows;
+        a.cell_cols = cell_cols;
+        a.d_codes = codes ? sl.d_codes : nullptr;
+        a.codes_img_stride = int64_t(img_bytes);
+        a.codes_pitch = pitch;
+        a.d_hist = hist32 ? sl.d_hist : nullptr;
+        s = lbp ? aldp_lbp_batch(&a, st) : aldp_ldp_batch(&a, st);
+        if (s != ALDP_OK) return hfail(s, aldp_last_error());
+        if (codes)
+            HOST_CUDA_TRY(cudaMemcpyAsync(c.h_codes.p, sl.d_codes, img_bytes * n, cudaMemcpyDeviceToHost, st));
+        if (hist32)
+            HOST_CUDA_TRY(cudaMemcpyAsync(c.h_hist.p, sl.d_hist, sizeof(uint32_t) * hist_per_img * n,
+                                          cudaMemcpyDeviceToHost, st));
+        HOST_CUDA_TRY(cudaStreamSynchronize(st));
+        if (codes) {
+            const uint8_t* hc = static_cast<const uint8_t*>(c.h_codes.p);
+            if (pitch == cols) {
+                std::memcpy(codes, hc, plane * n);
+            } else {
+                for (size_t r = 0; r < size_t(rows) * n; ++r) std::memcpy(codes + r * cols, hc + r * pitch, cols);
+            }
+        }
+        if (hist32) std::memcpy(hist32, c.h_hist.p, sizeof(uint32_t) * hist_per_img * n);
+        return ALDP_OK;
+    }
     // order the internal streams after work already queued on the caller's stream
     cudaEvent_t start = nullptr;
     if (user) {

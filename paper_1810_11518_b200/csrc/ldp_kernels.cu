@@ -271,9 +271,18 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
         p.cell_cols = a->cell_cols;
         p.grid_r = grid_r;
         p.grid_c = grid_c;
-        p.band_rows = a->cell_rows ? a->cell_rows : 128;
-        p.bands = (a->rows + p.band_rows - 1) / p.band_rows;
         p.blocks = (a->cols + kTileCols - 1) / kTileCols;
+        p.band_rows = a->cell_rows ? a->cell_rows : 128;
+        if (!a->cell_rows) {
+            // Small batches (a few frames per call): shorter bands until the
+            // tiles fill every warp slot once (2 tiles per warp, 2 CTAs of 8
+            // warps per SM); each band costs two recounted edge rows.
+            const int64_t slots = int64_t(n_sms()) * 2 * kFastWarps * 2;
+            while (p.band_rows > 16 &&
+                   int64_t(a->n_images) * ((a->rows + p.band_rows - 1) / p.band_rows) * p.blocks < slots)
+                p.band_rows /= 2;
+        }
+        p.bands = (a->rows + p.band_rows - 1) / p.band_rows;
         p.n_tiles = int64_t(a->n_images) * p.bands * p.blocks;
         p.one = 1;
         for (int id = 0; id < 64; ++id) p.id_code[id] = p.id_bin[id] = 0;
