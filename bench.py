@@ -204,27 +204,56 @@ def run_reference(args, cfg_name):
     return 0
 
 
+def host_info():
+    """nproc, CPU model, sockets, cores and hardware threads of this box."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        model, phys, cores, sibl = None, set(), {}, {}
+        cur = None
+        for line in open("/proc/cpuinfo"):
+            k, _, v = line.partition(":")
+            k, v = k.strip(), v.strip()
+            if k == "model name" and model is None:
+                model = v
+            elif k == "physical id":
+                cur = v
+                phys.add(v)
+            elif k == "cpu cores" and cur is not None:
+                cores[cur] = int(v)
+            elif k == "siblings" and cur is not None:
+                sibl[cur] = int(v)
+        info.update({"model": model, "sockets": len(phys) or 1,
+                     "cores": sum(cores.values()) or None, "threads": sum(sibl.values()) or None})
+    except OSError:
+        pass
+    return info
+
+
 def cpu_baseline(host_px, k, cr, cc):
-    """Reference library on this box's host cores, bounded sample."""
+    """Reference library on this box's host cores, bounded sample, timed with
+    the reference's own median_seconds (bench.cpp:51-78) when the reference
+    library is present."""
     import oracle
     threads = os.cpu_count() or 1
     kind = "reference" if oracle.have_ref() else "port"
-    fn = oracle.ref_batch if kind == "reference" else oracle.batch
     res = {}
     n = host_px.shape[0]
     for label, path, nthreads, count in (("aldp_all_cores", 1, threads, n), ("ldp_all_cores", 0, threads, n // 2),
                                          ("aldp_1_thread", 1, 1, max(1, n // threads)),
                                          ("ldp_1_thread", 0, 1, max(1, n // threads // 2))):
         sub = host_px[:max(count, 1)]
-        kw = {"path": path} if kind == "reference" else {}
-        t0 = time.perf_counter()
-        fn(sub, k=k, cell=(cr, cc), threads=nthreads, **kw)
-        dt = time.perf_counter() - t0
+        if kind == "reference":
+            dt = oracle.ref_median_seconds_batch(sub, k=k, cell=(cr, cc), path=path, threads=nthreads, repeats=3)
+        else:
+            t0 = time.perf_counter()
+            oracle.batch(sub, k=k, cell=(cr, cc), threads=nthreads)
+            dt = time.perf_counter() - t0
         res[label] = round(sub.size / dt / 1e6, 3)
     return {"value": res["aldp_all_cores"], "unit": "Mpixel/s", "cores": threads, "kind": kind,
             "sample": f"{n} images of {host_px.shape[1]}x{host_px.shape[2]} (first images of the "
-                      f"batch), ALDP/Accelerated, code map + histograms, {threads} threads",
-            "variants_mpx_s": res}
+                      f"batch), ALDP/Accelerated, code map + histograms, {threads} threads"
+                      + (", median of 3 (reference median_seconds)" if kind == "reference" else ""),
+            "variants_mpx_s": res, "host": host_info()}
 
 
 def main():
@@ -240,6 +269,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--kernel", default="auto", choices=["auto", "fast", "generic"])
+    ap.add_argument("--gather-chunks", type=int, default=2,
+                    help="N>1: split each rank's shard so chunk i's histogram gather overlaps chunk i+1's kernel")
     ap.add_argument("--force-dist", action="store_true",
                     help="initialise NCCL and run the histogram gather even at world size 1 (tests the path)")
     args = ap.parse_args()
@@ -304,12 +335,34 @@ def main():
                 gathered = [torch.empty_like(wire) for _ in range(world)]
     stream.synchronize()
 
-    def step():
-        aldp.ldp_batch(px, rows, cols, k=k, cell=(cr, cc), codes=codes, hist=hist,
-                       kernel=args.kernel, stream=sp)
+    # Chunks: with a gather (N > 1), chunk i's histograms travel on the comm
+    # stream while chunk i+1's kernel runs; a step ends when its last gather
+    # has landed, and the next step's kernels wait for that (hist reuse).
+    n_chunks = max(1, min(args.gather_chunks, mine)) if use_dist else 1
+    bounds = [(mine * i // n_chunks, mine * (i + 1) // n_chunks) for i in range(n_chunks)]
+    comm = torch.cuda.Stream(dev) if use_dist else None
+    chunk_ev = [torch.cuda.Event() for _ in bounds]
+    comm_done = torch.cuda.Event()
+
+    def launch_chunks():
+        for ci, (a, b) in enumerate(bounds):
+            aldp.ldp_batch(px[a:b], rows, cols, k=k, cell=(cr, cc), codes=codes[a:b], hist=hist[a:b],
+                           kernel=args.kernel, stream=sp)
+            if use_dist:
+                chunk_ev[ci].record(stream)
+                comm.wait_event(chunk_ev[ci])
+                with torch.cuda.stream(comm):
+                    gather_histograms(hist[a:b], dist, rank, world, wire=wire[a:b],
+                                      out=[g[a:b] for g in gathered] if rank == 0 else None)
+
+    def finish_step():
         if use_dist:
-            with torch.cuda.stream(stream):
-                gather_histograms(hist, dist, rank, world, wire=wire, out=gathered)
+            comm_done.record(comm)
+            stream.wait_event(comm_done)
+
+    def step():
+        launch_chunks()
+        finish_step()
 
     # ---- warmup ----
     for _ in range(args.warmup):
@@ -328,19 +381,18 @@ def main():
     t_start.record(stream)
     for i in range(args.steps):
         ev[2 * i].record(stream)
-        aldp.ldp_batch(px, rows, cols, k=k, cell=(cr, cc), codes=codes, hist=hist,
-                       kernel=args.kernel, stream=sp)
-        ev[2 * i + 1].record(stream)
-        if use_dist:
-            with torch.cuda.stream(stream):
-                gather_histograms(hist, dist, rank, world, wire=wire, out=gathered)
+        launch_chunks()
+        ev[2 * i + 1].record(stream)  # kernels only (the comm stream runs beside them)
+        finish_step()
     t_end.record(stream)
     torch.cuda.synchronize(dev)
     if use_dist:
         dist.barrier()
     clocks = sampler.stop()
     total_ms = t_start.elapsed_time(t_end)
-    launch_ms = sum(ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(args.steps)) / args.steps
+    launch_list = sorted(ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(args.steps))
+    launch_ms = sum(launch_list) / args.steps
+    launch_median_ms = launch_list[args.steps // 2]
     if use_dist:
         t = torch.tensor([total_ms, launch_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -348,6 +400,16 @@ def main():
     ms_per_step = total_ms / args.steps
     pixels = n * rows * cols
     value = pixels / (ms_per_step * 1e-3) / 1e6
+
+    # ---- output checksums (outside the timed region): identical at every N ----
+    w = torch.arange(1, nb + 1, device=dev, dtype=torch.int64)
+    h_sum = (hist.to(torch.int64) * w).sum()
+    c_sum = codes[:, :, :cols].to(torch.int64).sum()
+    sums = torch.stack([h_sum, c_sum])
+    if use_dist:
+        dist.all_reduce(sums)
+    checks = {"hist_weighted_sum": int(sums[0]), "code_sum": int(sums[1]),
+              "note": "sum over all images of bin-index-weighted counts, and of code bytes"}
 
     # ---- roofline of the dominant kernel (one launch = this rank's shard) ----
     hbm, peak_src = measured_peaks()
@@ -366,7 +428,8 @@ def main():
                    "k": k, "cell": [cr, cc], "parallelism": f"image shards x{world}",
                    "l2": "inputs larger than L2 (no flush)" if n * rows * cols > 4 * 126e6 else
                          "inputs smaller than L2: repeated steps hit L2",
-                   "kernel": args.kernel},
+                   "kernel": args.kernel, "gather_chunks": n_chunks,
+                   "checksums": checks},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                      "frac": round(achieved / hbm, 4),
                      "traffic": (round(traffic_bpp * mine * rows * cols / (launch_ms * 1e-3) / 1e9, 1)
@@ -375,9 +438,10 @@ def main():
                      "traffic_source": traffic_src,
                      "peak_source": peak_src,
                      "bytes_per_pixel": round(2.0 + bpp_hist, 4),
-                     "launch_ms": round(launch_ms, 4)},
+                     "launch_ms": round(launch_ms, 4), "launch_median_ms": round(launch_median_ms, 4),
+                     "launches_per_step": n_chunks},
         "clocks": clocks,
-        "gpu_launches": args.steps,
+        "gpu_launches": args.steps * n_chunks,
     }
 
     # ---- end to end through the host C-ABI (pinned host buffers) ----

@@ -357,3 +357,23 @@ def ref_bench_csv(series="images", size=0, counts=(1, 2, 4, 6, 8, 10), windows=(
                            buf, len(buf)):
         raise RuntimeError("reference bench failed")
     return buf.value.decode()
+
+
+def ref_median_seconds_batch(pixels, k: int = 3, cell=(0, 0), path: int = 1, threads: int = 1,
+                             repeats: int = 3) -> float:
+    """The reference's own timer (bench.cpp:51-78: warm-up pass, batches up to
+    >= 5 ms, median of `repeats`) around ref_batch (codes + histograms)."""
+    px = np.ascontiguousarray(pixels, dtype=np.uint8)
+    if px.ndim == 2:
+        px = px[None]
+    n, r, c = px.shape
+    nb = ref_n_bins(k)
+    cells = 1 if cell[0] == 0 else (r // cell[0]) * (c // cell[1])
+    codes = np.empty_like(px)
+    hist = np.empty((n, cells, nb), np.uint64)
+    return float(ref().ref_median_seconds_batch(px.ctypes.data, n, r, c, k, cell[0], cell[1], path,
+                                                 codes.ctypes.data, hist.ctypes.data, threads, repeats))
+
+
+def ref_n_bins(k: int) -> int:
+    return 256 if k == 0 else sum(1 for v in range(256) if bin(v).count("1") == k)

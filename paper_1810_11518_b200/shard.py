@@ -38,7 +38,7 @@ def gather_histograms(hist, dist, rank: int, world: int, wire=None, out: Optiona
     if wire is None:
         wire = torch.empty(hist.shape, dtype=torch.int16, device=hist.device)
     wire.copy_(hist)  # exact: counts < 65536 (wire_dtype_ok), int16 bit pattern
-    if world == 1:
+    if world == 1 and not (dist.is_available() and dist.is_initialized()):
         return [wire] if rank == 0 else None
     if rank == 0 and out is None:
         out = [torch.empty_like(wire) for _ in range(world)]

@@ -63,3 +63,52 @@ def test_gather_two_ranks(tmp_path):
     got = np.load(out)
     assert got.shape == want.shape
     assert np.array_equal(got.astype(np.uint64), want)
+
+
+def _chunked_worker(rank, world, port, images, result_path, n_chunks):
+    """bench.py's overlapped gather: each chunk of the shard is gathered into
+    views of rank 0's per-rank receive buffers."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    lo, hi = shard_range(images.shape[0], rank, world)
+    _, h = oracle.batch(images[lo:hi], k=3, cell=(8, 9), codes=False, threads=1)
+    hist = torch.from_numpy(h.astype(np.int32))
+    mine = hi - lo
+    wire = torch.empty(hist.shape, dtype=torch.int16)
+    gathered = [torch.empty_like(wire) for _ in range(world)] if rank == 0 else None
+    for c in range(n_chunks):
+        a, b = mine * c // n_chunks, mine * (c + 1) // n_chunks
+        gather_histograms(hist[a:b], dist, rank, world, wire=wire[a:b],
+                          out=[g[a:b] for g in gathered] if rank == 0 else None)
+    if rank == 0:
+        np.save(result_path, widen(gathered).numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_chunks", [1, 3])
+def test_chunked_gather_two_ranks(tmp_path, n_chunks):
+    rng = np.random.default_rng(1)
+    images = rng.integers(0, 256, size=(8, 20, 30), dtype=np.uint8)
+    out = str(tmp_path / "chunked.npy")
+    mp.spawn(_chunked_worker, args=(2, _free_port(), images, out, n_chunks), nprocs=2, join=True)
+    import oracle
+    _, want = oracle.batch(images, k=3, cell=(8, 9), codes=False)
+    assert np.array_equal(np.load(out).astype(np.uint64), want)
+
+
+def _single_rank_worker(rank, world, port, result_path):
+    """World size 1 with an initialised group still goes through dist.gather."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    h = torch.arange(2 * 3 * 4, dtype=torch.int32).view(2, 3, 4)
+    out = gather_histograms(h, dist, 0, 1)
+    np.save(result_path, widen(out).numpy())
+    dist.destroy_process_group()
+
+
+def test_gather_world_one_initialised(tmp_path):
+    out = str(tmp_path / "one.npy")
+    mp.spawn(_single_rank_worker, args=(1, _free_port(), out), nprocs=1, join=True)
+    assert np.array_equal(np.load(out), np.arange(24).reshape(2, 3, 4))
