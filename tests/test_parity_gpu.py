@@ -357,3 +357,24 @@ def test_lbp_host_entry_points():
     c, h = aldp.ldp_batch_host(batch, k=0, cell=(10, 14))
     wc, wh = oracle.batch(batch, k=0, cell=(10, 14))
     assert np.array_equal(c, wc) and np.array_equal(h.astype(np.uint64), wh)
+
+
+def test_host_entry_points_concurrent_threads():
+    """Every entry point may be called from several host threads at once
+    (per-thread streams and buffers; ctypes drops the GIL during the call)."""
+    from concurrent.futures import ThreadPoolExecutor
+    rng = np.random.default_rng(123)
+    imgs = [rng.integers(0, 256, size=(int(r), int(c)), dtype=np.uint8)
+            for r, c in rng.integers(3, 300, size=(48, 2))]
+    want = [oracle.histogram(im, 3) for im in imgs]
+    big = np.stack([oracle.make_random(96, 128, s) for s in range(40)])
+    want_big = oracle.batch(big, k=3, cell=(16, 32), codes=False)[1]
+
+    def job(i):
+        if i % 6 == 5:
+            _, h = aldp.ldp_batch_host(big, k=3, cell=(16, 32), codes=False)
+            return np.array_equal(h.astype(np.uint64), want_big)
+        return np.array_equal(aldp.ldp_histogram(imgs[i]), want[i])
+
+    with ThreadPoolExecutor(max_workers=8) as ex:
+        assert all(ex.map(job, range(len(imgs))))
