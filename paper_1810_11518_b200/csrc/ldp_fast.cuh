@@ -140,12 +140,14 @@ __device__ __forceinline__ uint32_t pair_id(const Col& a, const Col& b, const Co
 // result); four byte permutes in sign-replicate mode turn the eight result
 // bits per lane into 0x00/0xFF bytes, a select chain + fold packs them.
 // Returns the low pixel's code in byte 0 and the high pixel's in byte 1.
-__device__ __forceinline__ uint32_t pair_lbp(const Col& a, const Col& b, const Col& c) {
-    const uint32_t ctr = b.c;
+__device__ __forceinline__ uint32_t pair_lbp(const Col& a, const Col& b, const Col& c, uint32_t one) {
+    // 0x8000 - ctr per lane, once; the eight compares are then 2-input adds
+    // kept on the FMA pipe (the LBP kernel is ALU-bound)
+    const uint32_t nctr = 0x80008000u - b.c;
     const uint32_t r[8] = {a.l, a.c, a.r, b.r, c.r, c.c, c.l, b.l};
     uint32_t d[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) d[i] = r[i] + 0x80008000u - ctr;
+    for (int i = 0; i < 8; ++i) d[i] = fadd(r[i], nctr, one);
     // m = [lo bit i, hi bit i, lo bit i+1, hi bit i+1] as 0x00 / 0xFF bytes:
     // PTX prmt with selector nibbles 8|byte replicates the selected byte's
     // sign bit (__byte_perm masks that bit off, hence the inline PTX)
@@ -430,8 +432,8 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
 #pragma unroll
             for (int j = 0; j < NW; ++j) {
                 if constexpr (LBP) {
-                    X[2 * j] = pair_lbp(colA<SUMS>(a, j), colA<SUMS>(b, j), colA<SUMS>(c, j));
-                    X[2 * j + 1] = pair_lbp(colB<SUMS>(a, j), colB<SUMS>(b, j), colB<SUMS>(c, j));
+                    X[2 * j] = pair_lbp(colA<SUMS>(a, j), colA<SUMS>(b, j), colA<SUMS>(c, j), one);
+                    X[2 * j + 1] = pair_lbp(colB<SUMS>(a, j), colB<SUMS>(b, j), colB<SUMS>(c, j), one);
                 } else {
                     X[2 * j] = pair_id<K>(colA<SUMS>(a, j), colA<SUMS>(b, j), colA<SUMS>(c, j), one);
                     X[2 * j + 1] = pair_id<K>(colB<SUMS>(a, j), colB<SUMS>(b, j), colB<SUMS>(c, j), one);
@@ -592,7 +594,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
                 fetch(xs[0] + it + 2, xs[1] + it + 2, qn);  // next row in flight
                 constexpr uint32_t M = (NT - 1) * 4;
                 uint32_t X;
-                if constexpr (LBP) X = pair_lbp(wa, wb, wc);
+                if constexpr (LBP) X = pair_lbp(wa, wb, wc, one);
                 else X = pair_id<K>(wa, wb, wc, one);
                 red_shared(((X * 4u) & M) | (it < len[0] ? addr[0] : trash));
                 red_shared(((LBP ? X >> 6 : __umulhi(X, 1u << 18)) & M) | (it < len[1] ? addr[1] : trash));
