@@ -403,9 +403,10 @@ def main():
 
     # ---- output checksums (outside the timed region): identical at every N ----
     w = torch.arange(1, nb + 1, device=dev, dtype=torch.int64)
-    h_sum = (hist.to(torch.int64) * w).sum()
-    c_sum = codes[:, :, :cols].to(torch.int64).sum()
-    sums = torch.stack([h_sum, c_sum])
+    sums = torch.zeros(2, device=dev, dtype=torch.int64)
+    for a in range(0, mine, 2048):  # chunked: never materialise a widened copy of 20 GB
+        sums[0] += (hist[a:a + 2048].to(torch.int64) * w).sum()
+        sums[1] += codes[a:a + 2048, :, :cols].sum(dtype=torch.int64)
     if use_dist:
         dist.all_reduce(sums)
     checks = {"hist_weighted_sum": int(sums[0]), "code_sum": int(sums[1]),
