@@ -124,9 +124,18 @@ std::vector<unsigned char> read_file(const std::string& path) {
     std::FILE* f = std::fopen(path.c_str(), "rb");
     if (!f) pgm_fail(path, "cannot open file");
     std::vector<unsigned char> buf;
-    unsigned char chunk[1 << 16];
-    size_t n;
-    while ((n = std::fread(chunk, 1, sizeof chunk, f)) > 0) buf.insert(buf.end(), chunk, chunk + n);
+    long size = -1;
+    if (std::fseek(f, 0, SEEK_END) == 0) size = std::ftell(f);
+    if (size >= 0 && std::fseek(f, 0, SEEK_SET) == 0) {  // regular file: one sized read
+        buf.resize(size_t(size));
+        const size_t got = size ? std::fread(buf.data(), 1, buf.size(), f) : 0;
+        buf.resize(got);
+    } else {  // pipes and the like: read to EOF
+        std::clearerr(f);
+        unsigned char chunk[1 << 16];
+        size_t n;
+        while ((n = std::fread(chunk, 1, sizeof chunk, f)) > 0) buf.insert(buf.end(), chunk, chunk + n);
+    }
     const bool err = std::ferror(f);
     std::fclose(f);
     if (err) pgm_fail(path, "cannot open file");
@@ -178,21 +187,38 @@ void parse_payload(Cursor& in, const PgmHeader& h, const std::string& path, uint
     }
 }
 
-// One decoded file: dimensions + pixels (or the error it raised).
+// One decoded file: dimensions + pixels (or the error it raised). P5 keeps
+// the file buffer and points at its payload (no copy); P2 holds the parsed
+// pixels at offset 0.
 struct Loaded {
     int rows = 0, cols = 0;
-    std::vector<uint8_t> px;
+    std::vector<uint8_t> buf;
+    size_t offset = 0;
     std::string error;
+    const uint8_t* pixels() const { return buf.data() + offset; }
 };
 
 Loaded load_one(const std::string& path) {
     Loaded out;
     try {
-        const std::vector<unsigned char> buf = read_file(path);
-        Cursor in{buf.data(), buf.data() + buf.size()};
+        std::vector<unsigned char> file = read_file(path);
+        Cursor in{file.data(), file.data() + file.size()};
         const PgmHeader h = parse_header(in, path);
-        out.px.resize(size_t(h.rows) * h.cols);
-        parse_payload(in, h, path, out.px.data());
+        const size_t count = size_t(h.rows) * h.cols;
+        if (h.binary) {
+            const int sep = in.get();  // exactly one whitespace byte (pgm.cpp:91-95)
+            if (sep == EOF || !std::isspace(sep)) pgm_fail(path, "malformed header/payload separator");
+            if (size_t(in.end - in.p) < count) pgm_fail(path, "truncated pixel payload");
+            if (h.maxval < 255)
+                for (size_t i = 0; i < count; ++i)
+                    if (in.p[i] > h.maxval)
+                        pgm_fail(path, "pixel value " + std::to_string(in.p[i]) + " exceeds maxval");
+            out.offset = size_t(in.p - file.data());
+            out.buf = std::move(file);
+        } else {
+            out.buf.resize(count);
+            parse_payload(in, h, path, out.buf.data());
+        }
         out.rows = h.rows, out.cols = h.cols;
     } catch (const std::exception& e) {
         out.error = e.what();
@@ -200,15 +226,25 @@ Loaded load_one(const std::string& path) {
     return out;
 }
 
-std::vector<Loaded> load_parallel(const std::vector<std::string>& paths, size_t lo, size_t hi, int threads) {
-    std::vector<Loaded> out(hi - lo);
-    const int t = std::max(1, std::min<int>(threads, int(hi - lo)));
+// Runs fn(i) for i in [0, n) on up to `threads` host threads.
+template <typename F>
+void parallel_for(size_t n, int threads, F fn) {
+    const int t = int(std::max<size_t>(1, std::min<size_t>(size_t(std::max(threads, 1)), n)));
+    if (t == 1) {
+        for (size_t i = 0; i < n; ++i) fn(i);
+        return;
+    }
     std::vector<std::thread> pool;
     for (int w = 0; w < t; ++w)
         pool.emplace_back([&, w] {
-            for (size_t i = lo + w; i < hi; i += t) out[i - lo] = load_one(paths[i]);
+            for (size_t i = size_t(w); i < n; i += size_t(t)) fn(i);
         });
     for (auto& th : pool) th.join();
+}
+
+std::vector<Loaded> load_parallel(const std::vector<std::string>& paths, size_t lo, size_t hi, int threads) {
+    std::vector<Loaded> out(hi - lo);
+    parallel_for(hi - lo, threads, [&](size_t i) { out[i] = load_one(paths[lo + i]); });
     return out;
 }
 
@@ -454,33 +490,37 @@ void extract_files(const std::vector<std::string>& paths, Descriptor d, int wind
             }
             const size_t plane = size_t(rows) * cols;
             uint8_t* px = staging.get(plane * n);
-            for (size_t k = i; k < j; ++k) std::memcpy(px + (k - i) * plane, group[k].px.data(), plane);
+            parallel_for(size_t(n), threads, [&](size_t k) {
+                std::memcpy(px + k * plane, group[i + k].pixels(), plane);
+            });
             hist.resize(size_t(n) * cells * nb);
             const int cell = window > 0 ? window : 0;
             throw_status(d == Descriptor::Lbp
                              ? aldp_lbp_batch_host(px, n, rows, cols, cell, cell, nullptr, hist.data(), nullptr)
                              : aldp_ldp_batch_host(px, n, rows, cols, 3, cell, cell, nullptr, hist.data(), nullptr));
-            std::string text;
-            text.reserve(size_t(n) * cells * (nb * 4 + 64));
-            for (int k = 0; k < n; ++k) {
-                const std::string& id = paths[lo + i + size_t(k)];
+            // rows formatted per image on the pool, written in input order
+            std::vector<std::string> text(static_cast<size_t>(n));
+            parallel_for(size_t(n), threads, [&](size_t k) {
+                std::string& t = text[k];
+                const std::string& id = paths[lo + i + k];
+                t.reserve(size_t(cells) * (nb * 4 + id.size() + 16));
                 for (int64_t c = 0; c < cells; ++c) {
-                    text += id;
+                    t += id;
                     if (window > 0) {
-                        text += "#w";
-                        append_u64(text, uint64_t(c));
+                        t += "#w";
+                        append_u64(t, uint64_t(c));
                     }
-                    text += ',';
-                    text += name;
-                    const uint32_t* h = hist.data() + (size_t(k) * cells + c) * nb;
+                    t += ',';
+                    t += name;
+                    const uint32_t* h = hist.data() + (k * cells + c) * nb;
                     for (int b = 0; b < nb; ++b) {
-                        text += ',';
-                        append_u64(text, h[b]);
+                        t += ',';
+                        append_u64(t, h[b]);
                     }
-                    text += '\n';
+                    t += '\n';
                 }
-            }
-            out.write(text);
+            });
+            for (const std::string& t : text) out.write(t);
             i = j;
         }
     }
@@ -557,7 +597,7 @@ aldp_status aldp_load_pgm_batch(const char* const* paths, int n, int rows, int c
                                             std::to_string(rows) + " (width x height), got " +
                                             std::to_string(got[size_t(i)].cols) + "x" +
                                             std::to_string(got[size_t(i)].rows));
-            std::memcpy(out + size_t(i) * plane, got[size_t(i)].px.data(), plane);
+            std::memcpy(out + size_t(i) * plane, got[size_t(i)].pixels(), plane);
         }
     });
 }
