@@ -131,16 +131,24 @@ static aldp_status launch_fast_t(const FastParams& p, cudaStream_t st) {
     constexpr int NSEG = 32 / (kTileCols / (4 * NW));
     constexpr int REGION = K == 0 ? 1024 : kRegion;  // LBP: 256 counts per region
     const size_t smem = size_t(kFastWarps) * NSEG * kSegRegions * REGION + REGION;  // + alignment slack
-    static std::once_flag once;
-    static cudaError_t attr_err = cudaSuccess;
-    static int per_sm = 1;
-    std::call_once(once, [&] {
-        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        if (attr_err == cudaSuccess)
-            attr_err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFastWarps * 32, smem);
-        if (per_sm < 1) per_sm = 1;
+    // The shared-memory opt-in is a per-device function attribute: set it once
+    // per device this process launches on (several GPUs in one process work).
+    constexpr int kMaxDev = 64;
+    static std::once_flag once[kMaxDev];
+    static cudaError_t attr_err[kMaxDev];
+    static int per_sm_dev[kMaxDev];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDev) return cuda_fail(cudaErrorInvalidDevice, "fast kernel setup");
+    std::call_once(once[dev], [&] {
+        int ps = 1;
+        attr_err[dev] = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (attr_err[dev] == cudaSuccess)
+            attr_err[dev] = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, kFastWarps * 32, smem);
+        per_sm_dev[dev] = ps < 1 ? 1 : ps;
     });
-    if (attr_err != cudaSuccess) return cuda_fail(attr_err, "fast kernel setup");
+    if (attr_err[dev] != cudaSuccess) return cuda_fail(attr_err[dev], "fast kernel setup");
+    const int per_sm = per_sm_dev[dev];
     const int64_t warp_tiles = (p.n_tiles + NSEG - 1) / NSEG;
     const int64_t want = (warp_tiles + kFastWarps - 1) / kFastWarps;
     const int grid = int(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(per_sm) * n_sms())));
