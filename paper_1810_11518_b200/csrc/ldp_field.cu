@@ -308,9 +308,10 @@ __global__ void __launch_bounds__(256) response_field_row_kernel(const uint8_t* 
                     if constexpr (sizeof(OutT) == 2) {
                         *reinterpret_cast<uint4*>(p) = make_uint4(pk16(m[0], m[1]), pk16(m[2], m[3]),
                                                                   pk16(m[4], m[5]), pk16(m[6], m[7]));
-                    } else {
-                        reinterpret_cast<int4*>(p)[0] = make_int4(m[0], m[1], m[2], m[3]);
-                        reinterpret_cast<int4*>(p)[1] = make_int4(m[4], m[5], m[6], m[7]);
+                    } else {  // one 256-bit store per pixel (sm_100): a warp writes 1 KB contiguous
+                        asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(m[0]),
+                                     "r"(m[1]), "r"(m[2]), "r"(m[3]), "r"(m[4]), "r"(m[5]), "r"(m[6]), "r"(m[7])
+                                     : "memory");
                     }
                 }
                 A[k][0] = B[k][0], A[k][1] = B[k][1], A[k][2] = B[k][2];
@@ -481,8 +482,9 @@ static aldp_status field_launch(const uint8_t* d_px, int64_t img_stride, int row
     if (reinterpret_cast<uintptr_t>(d_out) % 16)
         return set_error(ALDP_EINVAL, "response field output must be 16-byte aligned");
     if (n == 0) return ALDP_OK;
+    // the row kernel's int32 stores are 256-bit: they need a 32-byte aligned output
     const bool bulk = pitch % 16 == 0 && img_stride % 16 == 0 && reinterpret_cast<uintptr_t>(d_px) % 16 == 0 &&
-                      !std::getenv("ALDP_FIELD_NOBULK");
+                      (!wide || reinterpret_cast<uintptr_t>(d_out) % 32 == 0) && !std::getenv("ALDP_FIELD_NOBULK");
     const bool naive = path == ALDP_PATH_NAIVE;
     if (bulk) {
         const int wchunk = std::min(cols, kRowChunk);
