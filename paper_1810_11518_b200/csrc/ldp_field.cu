@@ -245,7 +245,7 @@ __device__ __forceinline__ void issue_row_tile(const uint8_t* px, int64_t img_st
     }
 }
 
-template <bool NAIVE, typename OutT>
+template <bool NAIVE, typename OutT, bool PAIR = false>
 __global__ void __launch_bounds__(256) response_field_row_kernel(const uint8_t* __restrict__ px,
                                                                  int64_t img_stride, int pitch, int rows,
                                                                  int cols, int n_images, int stride,
@@ -276,9 +276,54 @@ __global__ void __launch_bounds__(256) response_field_row_kernel(const uint8_t* 
         const int b = i & 1;
         const RowTile g = row_tile(t, rows, cols);
         mbar_wait(&full[b], uint32_t((i >> 1) & 1));
+        const uint8_t* s = smem + b * buf_bytes;
+        if constexpr (PAIR) {
+            // int16 output, even width, 32 B aligned: thread owns column pairs
+            // (2q, 2q+1), q = tid + k*nt; one 256-bit store writes both
+            // pixels' vectors, so a warp stores 1 KB contiguous per pair slot
+            constexpr int KP = kRowCols / 2;
+            int off[KP][4], A[KP][4], B[KP][4];
+            bool okp[KP];
+#pragma unroll
+            for (int k = 0; k < KP; ++k) {
+                const int yl = 2 * (tid + k * nt);
+                okp[k] = yl + 1 < g.w;
+                const int y = g.y0 + min(yl, g.w - 2);
+                off[k][0] = max(y - 1, 0) - (g.y0 - 16);
+                off[k][1] = y - (g.y0 - 16);
+                off[k][2] = y + 1 - (g.y0 - 16);
+                off[k][3] = min(y + 2, cols - 1) - (g.y0 - 16);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) A[k][j] = s[off[k][j]], B[k][j] = s[stride + off[k][j]];
+            }
+            int16_t* o = reinterpret_cast<int16_t*>(out) + ((int64_t(g.img) * rows + g.x0) * cols + g.y0) * 8;
+            for (int r = 0; r < g.h; ++r, o += int64_t(cols) * 8) {
+                const uint8_t* sr = s + (r + 2) * stride;
+#pragma unroll
+                for (int k = 0; k < KP; ++k) {
+                    int C[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) C[j] = sr[off[k][j]];
+                    if (okp[k]) {
+                        const int r0[8] = {A[k][0], A[k][1], A[k][2], B[k][2], C[2], C[1], C[0], B[k][0]};
+                        const int r1[8] = {A[k][1], A[k][2], A[k][3], B[k][3], C[3], C[2], C[1], B[k][1]};
+                        int m[8], n[8];
+                        if constexpr (NAIVE) naive8(r0, m), naive8(r1, n);
+                        else identity8(r0, m), identity8(r1, n);
+                        int16_t* p = o + int64_t(2 * (tid + k * nt)) * 8;
+                        asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
+                                     "r"(pk16(m[0], m[1])), "r"(pk16(m[2], m[3])), "r"(pk16(m[4], m[5])),
+                                     "r"(pk16(m[6], m[7])), "r"(pk16(n[0], n[1])), "r"(pk16(n[2], n[3])),
+                                     "r"(pk16(n[4], n[5])), "r"(pk16(n[6], n[7]))
+                                     : "memory");
+                    }
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) A[k][j] = B[k][j], B[k][j] = C[j];
+                }
+            }
+        } else {
         // this thread's columns: y0 + tid + k*nt, k < kRowCols (warp-consecutive
         // pixels per k, so every 16 B store instruction writes 512 contiguous B)
-        const uint8_t* s = smem + b * buf_bytes;
         int cl[kRowCols], cm[kRowCols], cr[kRowCols];
         bool ok[kRowCols];
         int A[kRowCols][3], B[kRowCols][3];
@@ -317,6 +362,7 @@ __global__ void __launch_bounds__(256) response_field_row_kernel(const uint8_t* 
                 A[k][0] = B[k][0], A[k][1] = B[k][1], A[k][2] = B[k][2];
                 B[k][0] = c0, B[k][1] = c1, B[k][2] = c2;
             }
+        }
         }
         __syncthreads();  // buffer b fully read
         if (tid == 0) {
@@ -504,7 +550,13 @@ static aldp_status field_launch(const uint8_t* d_px, int64_t img_stride, int row
             naive ? go(response_field_row_kernel<true, int32_t>, o) : go(response_field_row_kernel<false, int32_t>, o);
         } else {
             auto* o = static_cast<int16_t*>(d_out);
-            naive ? go(response_field_row_kernel<true, int16_t>, o) : go(response_field_row_kernel<false, int16_t>, o);
+            const bool pair = cols % 2 == 0 && reinterpret_cast<uintptr_t>(d_out) % 32 == 0 &&
+                              !std::getenv("ALDP_FIELD_NOPAIR");
+            if (pair)
+                naive ? go(response_field_row_kernel<true, int16_t, true>, o)
+                      : go(response_field_row_kernel<false, int16_t, true>, o);
+            else
+                naive ? go(response_field_row_kernel<true, int16_t>, o) : go(response_field_row_kernel<false, int16_t>, o);
         }
     } else {
         const int64_t tiles =
