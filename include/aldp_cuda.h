@@ -78,6 +78,12 @@ typedef struct {
     int64_t codes_img_stride;
     int codes_pitch;
     uint32_t* d_hist;
+    /* 0 (default): every cell is clamped as an independent image, the
+     * reference's windowed_features semantics (windowing.cpp:42). 1: cells are
+     * cut from the whole-image code map (each pixel counted with its code-map
+     * code), the paper's "code image, then regional histograms" reading.
+     * Appended last so zero-initialised callers keep the reference rule. */
+    int cell_from_map;
 } aldp_ldp_args;
 
 aldp_status aldp_ldp_batch(const aldp_ldp_args* args, void* stream);

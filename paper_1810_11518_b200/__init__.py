@@ -88,6 +88,7 @@ class _Args(ctypes.Structure):
         ("cell_rows", ctypes.c_int), ("cell_cols", ctypes.c_int),
         ("d_codes", ctypes.c_void_p), ("codes_img_stride", ctypes.c_int64),
         ("codes_pitch", ctypes.c_int), ("d_hist", ctypes.c_void_p),
+        ("cell_from_map", ctypes.c_int),
     ]
 
 
@@ -295,20 +296,24 @@ _KERNEL = {"auto": 0, "fast": 1, "generic": 2}
 
 
 def lbp_batch(pixels, rows: int, cols: int, cell: Tuple[int, int] = (0, 0), codes=None, hist=None,
-              kernel: str = "auto", stream: Optional[int] = None):
+              kernel: str = "auto", stream: Optional[int] = None, cell_clamp: bool = True):
     """Device-resident LBP batch: like ldp_batch, hist [n, cells, 256]."""
     return ldp_batch(pixels, rows, cols, k=0, cell=cell, codes=codes, hist=hist, kernel=kernel,
-                     stream=stream)
+                     stream=stream, cell_clamp=cell_clamp)
 
 
 def ldp_batch(pixels, rows: int, cols: int, k: int = 3, cell: Tuple[int, int] = (0, 0),
-              codes=None, hist=None, kernel: str = "auto", stream: Optional[int] = None):
+              codes=None, hist=None, kernel: str = "auto", stream: Optional[int] = None,
+              cell_clamp: bool = True):
     """Device-resident batch (the hot path).
 
     pixels: torch.uint8 CUDA tensor [n, rows, pitch] (contiguous; pitch >= cols).
     codes:  None, True (allocate) or a torch.uint8 tensor [n, rows, codes_pitch].
     hist:   None, True (allocate) or a torch.int32/uint32 tensor [n, cells, n_bins].
     stream: a raw cudaStream_t (int); default: torch's current stream.
+    cell_clamp: True (the reference's windowed_features rule) clamps every
+            cell as its own image; False cuts cells from the whole-image code
+            map instead.
     Returns (codes, hist). Asynchronous on the stream.
     """
     import torch
@@ -330,6 +335,7 @@ def ldp_batch(pixels, rows: int, cols: int, k: int = 3, cell: Tuple[int, int] = 
     a.img_stride = rows * pitch
     a.rows, a.cols, a.pitch, a.n_images, a.k = rows, cols, pitch, n, int(k)
     a.cell_rows, a.cell_cols = int(cell[0]), int(cell[1])
+    a.cell_from_map = 0 if cell_clamp else 1
     if codes is not None:
         if codes.dtype != torch.uint8 or codes.dim() != 3 or not codes.is_contiguous():
             raise ValueError("codes must be a contiguous uint8 tensor [n, rows, pitch]")

@@ -60,6 +60,8 @@ struct FastParams {
     uint32_t* hist;
     int nbins;
     int cell_rows, cell_cols, grid_r, grid_c;  // cell mode only
+    int cell_clamp;                            // cell mode: 1 = per-cell clamp, 0 = cut from the code map
+    int edge_lo, edge_hi;                      // band rows recounted with the cell clamp (-1: none)
     int band_rows, bands, blocks;
     int64_t n_tiles;
     uint32_t one;         // 1 at run time: multiplier that keeps integer adds on the FMA pipe
@@ -402,7 +404,8 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
             int lc = 0;
             if (CELLS) {
                 const int cc = col / p.cell_cols, in = col - cc * p.cell_cols;
-                on = on && cc < p.grid_c && !(in == 0 && col > 0) && !(in == p.cell_cols - 1 && col < last);
+                on = on && cc < p.grid_c &&
+                     (!p.cell_clamp || (!(in == 0 && col > 0) && !(in == p.cell_cols - 1 && col < last)));
                 lc = cc - cell_c0;
             }
             slot[s] = on ? seg_base + uint32_t(lc) * REGION + CNT : trash;
@@ -470,10 +473,10 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
                 }
             }
             if (HIST) {
-                if (CELLS && (i == 0 || i == p.cell_rows - 1)) {
+                if (CELLS && (i == p.edge_lo || i == p.edge_hi)) {
                     // cell border row: count with the outside row clamped to the cell
                     uint32_t Y[NPAIR], bd[LC];
-                    row_ids(i == 0 ? b : a, b, i == p.cell_rows - 1 ? b : c, Y);
+                    row_ids(i == p.edge_lo ? b : a, b, i == p.edge_hi ? b : c, Y);
                     addrs(Y, bd);
                     if (live)
 #pragma unroll
@@ -512,7 +515,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
         else run_rows(std::integral_constant<bool, false>{});
 
         // ---- cell border columns: recount with the cell clamp ----
-        if (HIST && CELLS && __any_sync(FULL, do_hist)) {
+        if (HIST && CELLS && p.cell_clamp && __any_sync(FULL, do_hist)) {
             int* fl = fix_cols[warp][seg];
             if (sl == 0) {
                 int n = 0;

@@ -67,6 +67,7 @@ struct GenericParams {
     uint32_t* hist;
     int nbins;
     int cell_rows, cell_cols, grid_r, grid_c;  // cell_rows == 0: whole image
+    int cell_clamp;                            // 0: cells cut from the whole-image code map
 };
 
 __global__ void ldp_generic_kernel(GenericParams p) {
@@ -93,7 +94,7 @@ __global__ void ldp_generic_kernel(GenericParams p) {
             const bool edge = x == x0 || x == x0 + p.cell_rows - 1 || y == y0 ||
                               y == y0 + p.cell_cols - 1;
             unsigned hc = code;
-            if (edge)
+            if (edge && p.cell_clamp)
                 hc = p.k ? clamped_code(base, p.pitch, x, y, x0, x0 + p.cell_rows - 1, y0, y0 + p.cell_cols - 1, p.k)
                          : clamped_lbp(base, p.pitch, x, y, x0, x0 + p.cell_rows - 1, y0, y0 + p.cell_cols - 1);
             const int64_t cell = int64_t(img) * p.grid_r * p.grid_c + int64_t(cr) * p.grid_c + cc;
@@ -277,6 +278,9 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
         p.nbins = nbins;
         p.cell_rows = a->cell_rows;
         p.cell_cols = a->cell_cols;
+        p.cell_clamp = a->cell_from_map ? 0 : 1;
+        p.edge_lo = p.cell_clamp ? 0 : -1;
+        p.edge_hi = p.cell_clamp ? a->cell_rows - 1 : -1;
         p.grid_r = grid_r;
         p.grid_c = grid_c;
         p.blocks = (a->cols + kTileCols - 1) / kTileCols;
@@ -316,6 +320,7 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
     g.nbins = nbins;
     g.cell_rows = a->cell_rows;
     g.cell_cols = a->cell_cols;
+    g.cell_clamp = a->cell_from_map ? 0 : 1;
     g.grid_r = grid_r;
     g.grid_c = grid_c;
     const int64_t total = int64_t(a->rows) * a->cols * a->n_images;

@@ -378,3 +378,46 @@ def test_host_entry_points_concurrent_threads():
 
     with ThreadPoolExecutor(max_workers=8) as ex:
         assert all(ex.map(job, range(len(imgs))))
+
+
+def _hist_of_map(codes, k, cr, cc):
+    """Cells cut from a whole-image code map (numpy over the oracle's map)."""
+    n, r, c = codes.shape
+    gr, gc = r // cr, c // cc
+    if k == 0:
+        lut = np.arange(256)
+        nb = 256
+    else:
+        lut = np.full(256, -1)
+        ranks = [v for v in range(256) if bin(v).count("1") == k]
+        lut[ranks] = np.arange(len(ranks))
+        nb = len(ranks)
+    out = np.zeros((n, gr * gc, nb), np.uint64)
+    for i in range(n):
+        for a in range(gr):
+            for b in range(gc):
+                cell = lut[codes[i, a * cr:(a + 1) * cr, b * cc:(b + 1) * cc]].ravel()
+                out[i, a * gc + b] = np.bincount(cell, minlength=nb)
+    return out
+
+
+@pytest.mark.parametrize("k,cell", [(3, (16, 24)), (1, (81, 91)), (5, (7, 9)), (0, (32, 40)), (3, (3, 3))])
+def test_cells_cut_from_code_map(k, cell):
+    """cell_clamp=False: each cell histograms the whole-image code map
+    (the paper's regional histograms of one code image), both kernels."""
+    n, r, c = 3, 162, 184
+    px = aldp.gen_faces(n, r, c, seed=31 + k)
+    host = px[:, :, :c].cpu().numpy()
+    ref_codes, _ = oracle.batch(host, k=k, codes=True, hist=False)
+    want = _hist_of_map(ref_codes, k, *cell)
+    for kern in ("auto", "generic"):
+        fn = aldp.lbp_batch if k == 0 else aldp.ldp_batch
+        kw = {} if k == 0 else {"k": k}
+        codes, hist = fn(px, r, c, cell=cell, codes=True, hist=True, kernel=kern, cell_clamp=False, **kw)
+        torch.cuda.synchronize()
+        assert np.array_equal(codes[:, :, :c].cpu().numpy(), ref_codes), kern
+        assert np.array_equal(hist.cpu().numpy().astype(np.uint64), want), (kern, k, cell)
+        # and the default (reference windowed rule) is unchanged
+        _, h2 = fn(px, r, c, cell=cell, hist=True, kernel=kern, **kw)
+        torch.cuda.synchronize()
+        assert np.array_equal(h2.cpu().numpy().astype(np.uint64), oracle.batch(host, k=k, cell=cell, codes=False)[1])
