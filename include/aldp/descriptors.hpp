@@ -1,8 +1,8 @@
 // aldp/descriptors.hpp -- drop-in for the reference's
 // proj/include/aldp/descriptors.hpp (LDP part) plus the new code-map entry.
 // ldp_histogram and ldp_code_map run on the B200 through the C-ABI.
-#ifndef ALDP_DESCRIPTORS_HPP
-#define ALDP_DESCRIPTORS_HPP
+#ifndef ALDP_B200_DESCRIPTORS_HPP
+#define ALDP_B200_DESCRIPTORS_HPP
 
 #include <array>
 #include <cstdint>
@@ -58,4 +58,4 @@ std::vector<std::uint8_t> ldp_code_map(const GrayImage& img, int k = 3,
 
 }  // namespace aldp
 
-#endif  // ALDP_DESCRIPTORS_HPP
+#endif  // ALDP_B200_DESCRIPTORS_HPP
