@@ -16,6 +16,7 @@
 #include <cstdint>
 #include <cstring>
 #include <string>
+#include <thread>
 
 #include "aldp_cuda.h"
 
@@ -41,24 +42,7 @@ constexpr int kSlots = 3;
 constexpr size_t kChunkBytes = size_t(48) << 20;  // pixel bytes per chunk (~150 640x490 frames)
 constexpr size_t kSmallBytes = size_t(4) << 20;   // calls up to this many pixel bytes take the staged path
 
-struct Slot {
-    cudaStream_t stream = nullptr;
-    uint8_t* d_px = nullptr;
-    size_t px_cap = 0;
-    uint8_t* d_codes = nullptr;
-    size_t codes_cap = 0;
-    uint32_t* d_hist = nullptr;
-    size_t hist_cap = 0;
-    void release() {
-        if (d_px) cudaFree(d_px);
-        if (d_codes) cudaFree(d_codes);
-        if (d_hist) cudaFree(d_hist);
-        if (stream) cudaStreamDestroy(stream);
-        *this = Slot{};
-    }
-};
-
-// Pinned host staging for small calls (grow-only, per thread).
+// Pinned host staging (grow-only).
 struct PinnedBuf {
     void* p = nullptr;
     size_t cap = 0;
@@ -69,10 +53,33 @@ struct PinnedBuf {
     }
 };
 
+struct Slot {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t done = nullptr;  // staged path: the slot's chunk has landed in h_codes / h_hist
+    uint8_t* d_px = nullptr;
+    size_t px_cap = 0;
+    uint8_t* d_codes = nullptr;
+    size_t codes_cap = 0;
+    uint32_t* d_hist = nullptr;
+    size_t hist_cap = 0;
+    PinnedBuf h_px, h_codes, h_hist;  // staging for pageable caller buffers
+    void release() {
+        if (d_px) cudaFree(d_px);
+        if (d_codes) cudaFree(d_codes);
+        if (d_hist) cudaFree(d_hist);
+        if (stream) cudaStreamDestroy(stream);
+        if (done) cudaEventDestroy(done);
+        h_px.release();
+        h_codes.release();
+        h_hist.release();
+        *this = Slot{};
+    }
+};
+
 struct HostCtx {
     int device = -1;
     Slot slot[kSlots];
-    PinnedBuf h_px, h_codes, h_hist;
+    PinnedBuf h_px, h_codes, h_hist;  // small-call staging
     ~HostCtx() {
         // Process teardown: the CUDA context may already be gone; ignore errors.
         for (auto& s : slot) s.release();
@@ -109,13 +116,49 @@ static aldp_status ctx_ready(HostCtx& c) {
         c.h_px.release();
         c.h_codes.release();
         c.h_hist.release();
-        for (auto& s : c.slot) HOST_CUDA_TRY(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+        for (auto& s : c.slot) {
+            HOST_CUDA_TRY(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+            HOST_CUDA_TRY(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
+        }
         c.device = dev;
     }
     return ALDP_OK;
 }
 
 static int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+// Page-locked (or registered) host memory can be a DMA source/target as is.
+static bool is_pinned(const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
+// Copies `nrows` rows of `width` bytes between strided buffers on up to
+// kCopyThreads host threads (one thread moves ~8 GB/s; PCIe needs ~45).
+constexpr int kCopyThreads = 8;
+static void copy_rows(uint8_t* dst, size_t dst_pitch, const uint8_t* src, size_t src_pitch, size_t width,
+                      size_t nrows) {
+    const size_t bytes = width * nrows;
+    const int t = int(std::min<size_t>(kCopyThreads, std::max<size_t>(1, bytes >> 22)));  // >= 4 MB per thread
+    auto part = [&](size_t r0, size_t r1) {
+        if (dst_pitch == width && src_pitch == width) {
+            std::memcpy(dst + r0 * width, src + r0 * width, (r1 - r0) * width);
+        } else {
+            for (size_t r = r0; r < r1; ++r) std::memcpy(dst + r * dst_pitch, src + r * src_pitch, width);
+        }
+    };
+    if (t == 1) {
+        part(0, nrows);
+        return;
+    }
+    std::thread pool[kCopyThreads];
+    for (int i = 0; i < t; ++i) pool[i] = std::thread(part, nrows * i / t, nrows * (i + 1) / t);
+    for (int i = 0; i < t; ++i) pool[i].join();
+}
 
 // Shared body: host pixels (n contiguous rows x cols images) -> optional host
 // codes (contiguous) and u32 histograms `hist32` [n][cells][bins]. Pinned
@@ -214,16 +257,66 @@ static aldp_status host_batch(const uint8_t* px, int n, int rows, int cols, int 
         if (start) HOST_CUDA_TRY(cudaStreamWaitEvent(sl.stream, start, 0));
     }
     if (start) cudaEventDestroy(start);
+    // Pageable caller buffers go through per-slot pinned staging: the CPU
+    // copies chunk i+1 in and chunk i-1 out (pooled threads) while the GPU
+    // works on chunk i. Pinned ones are DMA'd directly.
+    const bool stage_px = !is_pinned(px);
+    const bool stage_codes = codes && !is_pinned(codes);
+    const bool stage_hist = hist32 && !is_pinned(hist32);
+    const bool staged = stage_px || stage_codes || stage_hist;
+    if (staged) {
+        for (int i = 0; i < used; ++i) {
+            Slot& sl = c.slot[i];
+            if (stage_px) s = ensure_pinned(sl.h_px, img_bytes * chunk);
+            if (s == ALDP_OK && stage_codes) s = ensure_pinned(sl.h_codes, img_bytes * chunk);
+            if (s == ALDP_OK && stage_hist) s = ensure_pinned(sl.h_hist, sizeof(uint32_t) * hist_per_img * chunk);
+            if (s != ALDP_OK) return s;
+        }
+    }
+    int pending[kSlots];  // chunk whose results wait in the slot's staging, or -1
+    for (int i = 0; i < kSlots; ++i) pending[i] = -1;
+    auto drain = [&](int slot_i) -> aldp_status {  // staged results of the slot's chunk -> caller
+        const int ch = pending[slot_i];
+        if (ch < 0) return ALDP_OK;
+        Slot& sl = c.slot[slot_i];
+        HOST_CUDA_TRY(cudaEventSynchronize(sl.done));
+        const int i0 = ch * chunk, cnt = std::min(chunk, n - i0);
+        if (stage_codes)
+            copy_rows(codes + size_t(i0) * plane, cols, static_cast<const uint8_t*>(sl.h_codes.p), pitch, cols,
+                      size_t(rows) * cnt);
+        if (stage_hist)
+            copy_rows(reinterpret_cast<uint8_t*>(hist32 + size_t(i0) * hist_per_img), 0,
+                      static_cast<const uint8_t*>(sl.h_hist.p), 0, sizeof(uint32_t) * hist_per_img * cnt, 1);
+        pending[slot_i] = -1;
+        return ALDP_OK;
+    };
     for (int ch = 0; ch < n_chunks; ++ch) {
-        Slot& sl = c.slot[ch % kSlots];
+        const int si = ch % kSlots;
+        Slot& sl = c.slot[si];
         const cudaStream_t st = sl.stream;
         const int i0 = ch * chunk, cnt = std::min(chunk, n - i0);
         const uint8_t* src = px + size_t(i0) * plane;
-        if (pitch == cols)
+        if (staged) {
+            // the slot's previous chunk out (its staging is about to be reused)
+            // and this chunk in, at the same time on separate copy pools; the
+            // previous H2D from h_px finished before that chunk's event fired
+            HOST_CUDA_TRY(cudaEventSynchronize(sl.done));
+            std::thread in;
+            if (stage_px)
+                in = std::thread(copy_rows, static_cast<uint8_t*>(sl.h_px.p), size_t(pitch), src, size_t(cols),
+                                 size_t(cols), size_t(rows) * cnt);
+            s = drain(si);
+            if (in.joinable()) in.join();
+            if (s != ALDP_OK) return s;
+        }
+        if (stage_px) {
+            HOST_CUDA_TRY(cudaMemcpyAsync(sl.d_px, sl.h_px.p, img_bytes * cnt, cudaMemcpyHostToDevice, st));
+        } else if (pitch == cols) {
             HOST_CUDA_TRY(cudaMemcpyAsync(sl.d_px, src, img_bytes * cnt, cudaMemcpyHostToDevice, st));
-        else
+        } else {
             HOST_CUDA_TRY(cudaMemcpy2DAsync(sl.d_px, pitch, src, cols, cols, size_t(rows) * cnt,
                                             cudaMemcpyHostToDevice, st));
+        }
         aldp_ldp_args a{};
         a.d_pixels = sl.d_px;
         a.img_stride = int64_t(img_bytes);
@@ -242,15 +335,27 @@ static aldp_status host_batch(const uint8_t* px, int n, int rows, int cols, int 
         if (s != ALDP_OK) return hfail(s, aldp_last_error());
         if (codes) {
             uint8_t* dst = codes + size_t(i0) * plane;
-            if (pitch == cols)
+            if (stage_codes)
+                HOST_CUDA_TRY(cudaMemcpyAsync(sl.h_codes.p, sl.d_codes, img_bytes * cnt, cudaMemcpyDeviceToHost, st));
+            else if (pitch == cols)
                 HOST_CUDA_TRY(cudaMemcpyAsync(dst, sl.d_codes, img_bytes * cnt, cudaMemcpyDeviceToHost, st));
             else
                 HOST_CUDA_TRY(cudaMemcpy2DAsync(dst, cols, sl.d_codes, pitch, cols, size_t(rows) * cnt,
                                                 cudaMemcpyDeviceToHost, st));
         }
-        if (hist32)
-            HOST_CUDA_TRY(cudaMemcpyAsync(hist32 + size_t(i0) * hist_per_img, sl.d_hist,
-                                          sizeof(uint32_t) * hist_per_img * cnt, cudaMemcpyDeviceToHost, st));
+        if (hist32) {
+            void* hdst = stage_hist ? sl.h_hist.p : static_cast<void*>(hist32 + size_t(i0) * hist_per_img);
+            HOST_CUDA_TRY(cudaMemcpyAsync(hdst, sl.d_hist, sizeof(uint32_t) * hist_per_img * cnt,
+                                          cudaMemcpyDeviceToHost, st));
+        }
+        if (staged) {
+            HOST_CUDA_TRY(cudaEventRecord(sl.done, st));
+            pending[si] = ch;
+        }
+    }
+    for (int i = 0; i < used; ++i) {
+        s = drain(i);
+        if (s != ALDP_OK) return s;
     }
     for (int i = 0; i < used; ++i) HOST_CUDA_TRY(cudaStreamSynchronize(c.slot[i].stream));
     return ALDP_OK;
