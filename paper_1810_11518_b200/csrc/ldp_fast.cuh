@@ -414,9 +414,12 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
         uint8_t* const lane_dst =
             CODES ? p.codes + int64_t(img) * p.codes_img_stride + int64_t(r0) * p.codes_pitch + y : nullptr;
         const bool lane_out = seg_live && y < p.cols;
+        // widths that are not a multiple of the lane's 4*NW columns: the lane
+        // holding the last column stores its valid bytes one by one
+        const bool lane_full = lane_out && y + LC <= p.cols;
         // Common case: every lane of the warp is inside the image and on a
         // live row of equal-height tiles -> no per-lane predication at all.
-        const bool simple = __all_sync(FULL, lane_out && seg_rows == n_rows);
+        const bool simple = __all_sync(FULL, lane_full && seg_rows == n_rows);
 
         // Slot addresses of the lane's pixel ids. Pair q = 2j (P_A of word
         // j) covers columns y+4j (lo) / y+4j+2 (hi); q = 2j+1 (P_B) covers
@@ -466,10 +469,13 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
                     for (int j = 0; j < NW; ++j)  // bytes -> word with multiply-adds (FMA pipe)
                         wd[j] = e[4 * j] + e[4 * j + 1] * 0x100u + e[4 * j + 2] * 0x10000u + e[4 * j + 3] * 0x1000000u;
                 }
-                if (SIMPLE || (live && lane_out)) {
+                if (SIMPLE || (live && lane_full)) {
                     uint8_t* o = lane_dst + (long long)i * p.codes_pitch;
                     if constexpr (NW == 1) *reinterpret_cast<uint32_t*>(o) = wd[0];
                     else *reinterpret_cast<uint2*>(o) = make_uint2(wd[0], wd[1]);
+                } else if (live && lane_out) {
+                    uint8_t* o = lane_dst + (long long)i * p.codes_pitch;
+                    for (int b = 0; b < p.cols - y; ++b) o[b] = uint8_t(wd[b >> 2] >> (8 * (b & 3)));
                 }
             }
             if (HIST) {

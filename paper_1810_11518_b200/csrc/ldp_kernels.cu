@@ -253,7 +253,7 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
     const int nw = lane_words();
     const int al = 4 * nw;  // alignment the per-lane vector loads/stores need
     const bool aligned =
-        a->cols % 4 == 0 && a->pitch % al == 0 && (a->n_images <= 1 || a->img_stride % al == 0) &&
+        a->pitch % al == 0 && (a->n_images <= 1 || a->img_stride % al == 0) &&
         (reinterpret_cast<uintptr_t>(a->d_pixels) % al) == 0 &&
         (!a->d_codes || (a->codes_pitch % al == 0 && (reinterpret_cast<uintptr_t>(a->d_codes) % al) == 0 &&
                          (a->n_images <= 1 || a->codes_img_stride % al == 0)));
@@ -261,7 +261,7 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
     if (a->cell_rows) ncl = max_cells_per_tile(a->cols, a->cell_cols, grid_c);
     const bool fast_ok = aligned && k != 4 && ncl <= kMaxTileCells;
     if (kernel == ALDP_KERNEL_FAST && !fast_ok)
-        return fail(ALDP_EINVAL, "fast kernel needs cols % 4 == 0, aligned pitches/strides, "
+        return fail(ALDP_EINVAL, "fast kernel needs 8-byte aligned pitches/strides, "
                                  "k != 4 and at most 5 cells per 128 columns");
     if (kernel != ALDP_KERNEL_GENERIC && fast_ok) {
         FastParams p{};

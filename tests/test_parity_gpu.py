@@ -421,3 +421,29 @@ def test_cells_cut_from_code_map(k, cell):
         _, h2 = fn(px, r, c, cell=cell, hist=True, kernel=kern, **kw)
         torch.cuda.synchronize()
         assert np.array_equal(h2.cpu().numpy().astype(np.uint64), oracle.batch(host, k=k, cell=cell, codes=False)[1])
+
+
+@pytest.mark.parametrize("cols", [3, 5, 7, 13, 29, 127, 129, 130, 133, 255, 257, 490])
+def test_fast_kernel_any_width(cols):
+    """The packed kernel takes widths that are not a multiple of its 8-column
+    lanes (the edge lane stores its valid bytes singly; padding untouched)."""
+    rng = np.random.default_rng(cols)
+    rows = 37
+    img = rng.integers(0, 256, size=(3, rows, cols), dtype=np.uint8)
+    for k in (3, 5):
+        want_c, want_h = oracle.batch(img, k=k)
+        c, h = run(img, k, kernel="fast")
+        assert np.array_equal(c, want_c) and np.array_equal(h, want_h), (cols, k)
+    if cols >= 9:
+        cell = (9, max(3, cols // 3))
+        want_c, want_h = oracle.batch(img, k=3, cell=cell)
+        c, h = run(img, 3, cell=cell, kernel="fast")
+        assert np.array_equal(c, want_c) and np.array_equal(h, want_h), (cols, cell)
+    # bytes past `cols` inside the pitch are never written
+    d = to_dev(img)
+    pitch = d.shape[2]
+    codes = torch.full((3, rows, pitch), 0xAB, dtype=torch.uint8, device=DEV)
+    aldp.ldp_batch(d, rows, cols, k=3, codes=codes, kernel="fast")
+    torch.cuda.synchronize()
+    if pitch > cols:
+        assert bool((codes[:, :, cols:] == 0xAB).all())
