@@ -7,18 +7,26 @@ histograms (cells 81 x 91, per-cell clamp = windowed_features semantics).
 The batch is sharded by image across ranks (one process per GPU); each rank
 generates its shard on device keyed by global image index, so every N sees
 identical bytes. With N > 1 the per-image cell histograms are gathered to
-rank 0 (NCCL) inside the timed step. Total work is fixed -> "strong".
+rank 0 (NCCL, uint16 on the wire) inside the timed step, overlapped with the
+kernels in --gather-chunks pieces on a comm stream. Total work is fixed ->
+"strong". --force-dist runs the NCCL path at world size 1.
 
 A "step" is one pass of the LDP path over the whole batch. Inputs (20.6 GB)
 far exceed L2 (126 MB), so no L2 flush is needed between steps.
 
-  value   : whole-job Mpixel/s, device-resident inputs, CUDA events, max over ranks
+  value   : whole-job Mpixel/s, device-resident inputs, CUDA events on the
+            launching stream, max over ranks (20 timed steps by default)
   e2e     : same metric through the host C-ABI entry point (aldp_ldp_batch_host)
-            from pinned host memory: H2D pixels + kernel + D2H codes + D2H hist
+            from pinned host memory: H2D pixels + kernel + D2H codes + D2H hist,
+            every rank at once through its own PCIe link, max over ranks
   roofline: algorithmic bytes (1 B in + 1 B code + 4 B x 42 x 56 hist per image)
-            per launch / average launch time, vs MEASURED_PEAKS.json hbm_gbs
+            per launch / average launch time, vs MEASURED_PEAKS.json hbm_gbs;
+            traffic = ncu DRAM bytes per pixel (profiles/traffic.json) at that rate
+  clocks  : nvidia-smi samples during the timed region
+  checksums: bin-weighted histogram sum and code-byte sum (identical at any N)
   cpu_baseline: the reference library (oracle/_ref, unmodified reference
-            sources) on this box's host cores, bounded sample
+            sources) on this box's host cores, bounded sample, timed with the
+            reference's own median_seconds; host CPU described
 
 `--impl reference` times the reference's own CPU implementation (oracle/_ref,
 Accelerated path, all host threads) on a bounded sample per step; rank 0 only.
