@@ -103,3 +103,22 @@ def test_shard_invariance_c5_slice():
     _, h1 = aldp.ldp_batch(hi, r, c, k=3, cell=(81, 91), hist=True)
     torch.cuda.synchronize()
     assert torch.equal(torch.cat([h0, h1]), h)
+
+
+def test_config5_full_batch_sampled_vs_oracle():
+    """Config 5 at full size: all 65,536 frames (20.6 GB) in one launch, as
+    bench.py runs it; 48 frames at a stride across the batch checked
+    bit-exactly against the CPU oracle (codes and 7x6 cell histograms), and
+    every cell's mass checked for all frames."""
+    n, r, c = 65536, 490, 640
+    d = aldp.gen_faces(n, r, c, seed=11518)
+    codes, hist = aldp.ldp_batch(d, r, c, k=3, cell=(81, 91), codes=True, hist=True)
+    torch.cuda.synchronize()
+    assert bool((hist.sum(dim=2) == 81 * 91).all())
+    idx = list(range(0, n, n // 47))[:47] + [n - 1]
+    host = d[idx].cpu().numpy()
+    want_c, want_h = oracle.batch(host, k=3, cell=(81, 91), threads=16)
+    assert np.array_equal(codes[idx].cpu().numpy(), want_c)
+    assert np.array_equal(hist[idx].cpu().numpy().astype(np.uint64), want_h)
+    del codes, hist, d
+    torch.cuda.empty_cache()
