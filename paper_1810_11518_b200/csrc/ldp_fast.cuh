@@ -269,14 +269,26 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
     // warp then takes the predicate-free path. Neighbouring bands of an image
     // stay close in time, so band halos hit L2.
     const int G = (p.blocks & 1) ? 2 : 1;
+    // 32-bit index math whenever the tile count allows it (a 64-bit divide
+    // is a ~100-instruction software routine; this runs 3x per tile)
+    const bool small_t = p.n_tiles < (int64_t(1) << 30);
+    const uint32_t group_tiles = uint32_t(G * tiles_per_image);
     auto tile_coords = [&](int64_t tt, int& img_, int& band_, int& blk_) {
-        const int64_t grp = tt / (G * tiles_per_image);
-        const int64_t t_in = tt - grp * G * tiles_per_image;
+        int64_t grp;
+        uint32_t t_in;
+        if (small_t) {
+            const uint32_t q = uint32_t(tt) / group_tiles;
+            grp = q;
+            t_in = uint32_t(tt) - q * group_tiles;
+        } else {
+            grp = tt / (G * tiles_per_image);
+            t_in = uint32_t(tt - grp * G * tiles_per_image);
+        }
         const int64_t left_ = p.n_images - grp * G;
         const int gi = left_ < G ? int(left_) : G;  // images in this group
-        const int per_band = gi * p.blocks;
+        const uint32_t per_band = uint32_t(gi * p.blocks);
         band_ = int(t_in / per_band);
-        const int rem_ = int(t_in - int64_t(band_) * per_band);
+        const int rem_ = int(t_in - uint32_t(band_) * per_band);
         img_ = int(grp * G) + rem_ / p.blocks;
         blk_ = rem_ % p.blocks;
     };
