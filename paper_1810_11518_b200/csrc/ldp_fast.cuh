@@ -409,13 +409,16 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
         // ---- histogram slots: region address per pixel (or trash) ----
         const int cell_c0 = CELLS ? c0 / p.cell_cols : 0;
         uint32_t slot[LC];
+        // one divide per lane: the lane's columns are consecutive, so the
+        // cell index / in-cell offset advance by carries (cell_cols >= 3)
+        int cc = CELLS ? y / p.cell_cols : 0, in = CELLS ? y - cc * p.cell_cols : 0;
 #pragma unroll
         for (int s = 0; s < LC; ++s) {
             const int col = y + s;
             bool on = do_hist && col < p.cols;
             int lc = 0;
             if (CELLS) {
-                const int cc = col / p.cell_cols, in = col - cc * p.cell_cols;
+                if (s > 0 && ++in == p.cell_cols) in = 0, ++cc;
                 on = on && cc < p.grid_c &&
                      (!p.cell_clamp || (!(in == 0 && col > 0) && !(in == p.cell_cols - 1 && col < last)));
                 lc = cc - cell_c0;
