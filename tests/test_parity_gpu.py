@@ -434,7 +434,7 @@ def test_fast_kernel_any_width(cols):
         want_c, want_h = oracle.batch(img, k=k)
         c, h = run(img, k, kernel="fast")
         assert np.array_equal(c, want_c) and np.array_equal(h, want_h), (cols, k)
-    if cols >= 9:
+    if cols >= 3:
         cell = (9, max(3, cols // 3))
         want_c, want_h = oracle.batch(img, k=3, cell=cell)
         c, h = run(img, 3, cell=cell, kernel="fast")
