@@ -175,8 +175,15 @@ def run_reference(args, cfg_name):
         return 0
     n, rows, cols, k, cr, cc, blobs, gen, seed = CONFIGS[cfg_name]
     threads = os.cpu_count() or 1
-    sample = max(threads * 4, 32) if cfg_name in ("c5", "c2", "c5w", "c5lbp") else 1
-    if gen == "faces":
+    sample = max(threads * 4, 32) if cfg_name in ("c5", "c2", "c5w", "c5lbp") else \
+        (threads if cfg_name == "c3" else 1)
+    if gen == "faces" and rows * cols >= 1e8:
+        # C4: a band of the 16384^2 frame (1024 rows), cut into one row band of
+        # whole 64-row cells per host thread -- cells are clamped independently,
+        # so the bands are exactly the frame's work for those rows
+        band = numpy_faces(1, 1024, cols, max(1, blobs // 16), seed)[0]
+        px = band.reshape(1024 // cr, cr, cols) if cr else band[None]
+    elif gen == "faces":
         px = numpy_faces(sample, rows, cols, blobs, seed)
     elif gen == "ties":
         rng = np.random.default_rng(seed)
@@ -202,7 +209,7 @@ def run_reference(args, cfg_name):
         "config": {"workload": WORKLOAD_NAMES[cfg_name], "images_per_step": int(px.shape[0]),
                    "parallelism": f"{threads} host threads over images", "cpu_only": True},
         "cpu_baseline": {"value": round(mpx, 3), "unit": "Mpixel/s", "cores": threads, "kind": kind,
-                         "sample": f"{px.shape[0]} images of {rows}x{cols} per step, "
+                         "sample": f"{px.shape[0]} images of {px.shape[1]}x{px.shape[2]} per step, "
                                    f"{'LBP' if k == 0 else 'ALDP (ResponsePath::Accelerated)'}, "
                                    f"code map + histograms"},
         "e2e": {"value": round(mpx, 3), "unit": "Mpixel/s", "h2d_bytes_per_step": 0,
@@ -258,7 +265,7 @@ def cpu_baseline(host_px, k, cr, cc):
             dt = time.perf_counter() - t0
         res[label] = round(sub.size / dt / 1e6, 3)
     return {"value": res["aldp_all_cores"], "unit": "Mpixel/s", "cores": threads, "kind": kind,
-            "sample": f"{n} images of {host_px.shape[1]}x{host_px.shape[2]} (first images of the "
+            "sample": f"{n} images of {host_px.shape[1]}x{host_px.shape[2]} (taken from the start of the "
                       f"batch), ALDP/Accelerated, code map + histograms, {threads} threads"
                       + (", median of 3 (reference median_seconds)" if kind == "reference" else ""),
             "variants_mpx_s": res, "host": host_info()}
@@ -501,12 +508,16 @@ def main():
 
     # ---- CPU baseline (reference library on this box's host cores) ----
     if not args.no_cpu and rank == 0 and world == 1:
-        cpu_n = args.cpu_images or (min(mine, 4 * (os.cpu_count() or 1) * 8) if rows * cols < 1e6 else 1)
-        host = px[:cpu_n, :, :cols].cpu().numpy()
-        if rows * cols >= 1e8:  # C4: a bounded row band of the big frame
-            host = host[:, :2048, :]
-        line["cpu_baseline"] = cpu_baseline(host, k, cr if rows * cols < 1e8 else cr,
-                                            cc if rows * cols < 1e8 else cc)
+        threads = os.cpu_count() or 1
+        if rows * cols >= 1e8:
+            # C4: a 2048-row band of the frame, split into bands of whole cells
+            # (one per host thread) so every core works on it
+            band = px[0, :2048, :cols].cpu().numpy()
+            host = band.reshape(2048 // cr, cr, cols) if cr else band[None]
+        else:
+            cpu_n = args.cpu_images or (min(mine, 4 * threads * 8) if rows * cols < 1e6 else min(mine, threads))
+            host = px[:cpu_n, :, :cols].cpu().numpy()
+        line["cpu_baseline"] = cpu_baseline(host, k, cr, cc)
     if rank == 0:
         sys.stdout.flush()
         os.write(out_fd, (json.dumps(line) + "\n").encode())
