@@ -84,6 +84,12 @@ typedef struct {
      * code), the paper's "code image, then regional histograms" reading.
      * Appended last so zero-initialised callers keep the reference rule. */
     int cell_from_map;
+    /* Rows of a larger resident image that exist above row 0 / below the last
+     * row of this view (0 or 1; default 0 = clamp at the view's edges). With 1
+     * the view's edge rows see the real neighbour row instead of a clamped
+     * copy, so a tall frame can be processed as bands with identical codes
+     * and histograms (cells must then start at a multiple of cell_rows). */
+    int rows_above, rows_below;
 } aldp_ldp_args;
 
 aldp_status aldp_ldp_batch(const aldp_ldp_args* args, void* stream);

@@ -88,7 +88,7 @@ class _Args(ctypes.Structure):
         ("cell_rows", ctypes.c_int), ("cell_cols", ctypes.c_int),
         ("d_codes", ctypes.c_void_p), ("codes_img_stride", ctypes.c_int64),
         ("codes_pitch", ctypes.c_int), ("d_hist", ctypes.c_void_p),
-        ("cell_from_map", ctypes.c_int),
+        ("cell_from_map", ctypes.c_int), ("rows_above", ctypes.c_int), ("rows_below", ctypes.c_int),
     ]
 
 
@@ -304,7 +304,7 @@ def lbp_batch(pixels, rows: int, cols: int, cell: Tuple[int, int] = (0, 0), code
 
 def ldp_batch(pixels, rows: int, cols: int, k: int = 3, cell: Tuple[int, int] = (0, 0),
               codes=None, hist=None, kernel: str = "auto", stream: Optional[int] = None,
-              cell_clamp: bool = True):
+              cell_clamp: bool = True, halo: Tuple[int, int] = (0, 0)):
     """Device-resident batch (the hot path).
 
     pixels: torch.uint8 CUDA tensor [n, rows, pitch] (contiguous; pitch >= cols).
@@ -314,6 +314,9 @@ def ldp_batch(pixels, rows: int, cols: int, k: int = 3, cell: Tuple[int, int] = 
     cell_clamp: True (the reference's windowed_features rule) clamps every
             cell as its own image; False cuts cells from the whole-image code
             map instead.
+    halo:   (above, below) in {0, 1}: real image rows exist just above / below
+            this view (pixels is a band of a taller resident frame), so the
+            view's edge rows see them instead of a clamped copy.
     Returns (codes, hist). Asynchronous on the stream.
     """
     import torch
@@ -336,6 +339,7 @@ def ldp_batch(pixels, rows: int, cols: int, k: int = 3, cell: Tuple[int, int] = 
     a.rows, a.cols, a.pitch, a.n_images, a.k = rows, cols, pitch, n, int(k)
     a.cell_rows, a.cell_cols = int(cell[0]), int(cell[1])
     a.cell_from_map = 0 if cell_clamp else 1
+    a.rows_above, a.rows_below = int(bool(halo[0])), int(bool(halo[1]))
     if codes is not None:
         if codes.dtype != torch.uint8 or codes.dim() != 3 or not codes.is_contiguous():
             raise ValueError("codes must be a contiguous uint8 tensor [n, rows, pitch]")

@@ -188,7 +188,7 @@ __device__ __forceinline__ unsigned clamped_code(const uint8_t* img, int pitch, 
     for (int j = 0; j < 8; ++j) {
         const int xx = min(max(x + ring_dx(j), x_lo), x_hi);
         const int yy = min(max(y + ring_dy(j), y_lo), y_hi);
-        r[j] = __ldg(img + size_t(xx) * size_t(pitch) + size_t(yy));
+        r[j] = __ldg(img + int64_t(xx) * pitch + yy);  // xx may be -1 (halo row of a band view)
     }
     return ring_code(r, k);
 }
@@ -203,7 +203,7 @@ __device__ __forceinline__ unsigned clamped_lbp(const uint8_t* img, int pitch, i
     for (int j = 0; j < 8; ++j) {
         const int xx = min(max(x + ring_dx(j), x_lo), x_hi);
         const int yy = min(max(y + ring_dy(j), y_lo), y_hi);
-        code |= unsigned(__ldg(img + size_t(xx) * size_t(pitch) + size_t(yy)) >= ctr) << j;
+        code |= unsigned(__ldg(img + int64_t(xx) * pitch + yy) >= ctr) << j;
     }
     return code;
 }

@@ -62,6 +62,7 @@ struct FastParams {
     int cell_rows, cell_cols, grid_r, grid_c;  // cell mode only
     int cell_clamp;                            // cell mode: 1 = per-cell clamp, 0 = cut from the code map
     int edge_lo, edge_hi;                      // band rows recounted with the cell clamp (-1: none)
+    int row_lo, row_hi;                        // rows readable as neighbours (-1 / rows with halos)
     int band_rows, bands, blocks;
     int64_t n_tiles;
     uint32_t one;         // 1 at run time: multiplier that keeps integer adds on the FMA pipe
@@ -363,7 +364,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
         const uint8_t* const halo_p = img_px + halo_off;
         const uint8_t* const pf_p = img_px + c0;
         auto load_raw = [&](int r) -> RawN<NW> {
-            const int rr = min(max(r, 0), p.rows - 1);
+            const int rr = min(max(r, p.row_lo), p.row_hi);
             if (!CELLS && sl == 1) {  // pull a row further ahead into L2 (measured: pays only without cells)
                 const int ra_ = min(r + kL2Ahead, p.rows - 1);
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(pf_p + (long long)ra_ * p.pitch));

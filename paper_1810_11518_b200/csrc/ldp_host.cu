@@ -16,6 +16,7 @@
 #include <cstdint>
 #include <cstring>
 #include <string>
+#include <vector>
 #include <thread>
 
 #include "aldp_cuda.h"
@@ -40,6 +41,16 @@ static aldp_status hfail(aldp_status s, const std::string& msg) { return set_err
 // (separate copy engines per direction; stream order protects buffer reuse).
 constexpr int kSlots = 3;
 constexpr size_t kChunkBytes = size_t(48) << 20;  // pixel bytes per chunk (~150 640x490 frames)
+// ALDP_CHUNK_BYTES overrides the chunk size (tests drive the banded and
+// chunked paths with small inputs through it)
+static size_t chunk_bytes() {
+    static const size_t v = [] {
+        const char* e = std::getenv("ALDP_CHUNK_BYTES");
+        const long long x = e ? std::atoll(e) : 0;
+        return x > 0 ? size_t(x) : kChunkBytes;
+    }();
+    return v;
+}
 constexpr size_t kSmallBytes = size_t(4) << 20;   // calls up to this many pixel bytes take the staged path
 
 // Pinned host staging (grow-only).
@@ -160,6 +171,135 @@ static void copy_rows(uint8_t* dst, size_t dst_pitch, const uint8_t* src, size_t
     for (int i = 0; i < t; ++i) pool[i].join();
 }
 
+// Tall single frame in bands (see host_batch). Band b covers rows
+// [b*B, min(rows, (b+1)*B)); B is a multiple of cell_rows so every cell lies
+// in one band and the band's cells are a contiguous run of the frame's grid.
+// Pageable pixels and codes go through pinned staging (the copy in also
+// assembles the halo rows and the device pitch); pinned ones are DMA'd.
+static aldp_status host_band(HostCtx& c, const uint8_t* px, int rows, int cols, int k, int cell_rows,
+                             int cell_cols, uint8_t* codes, uint32_t* hist32, bool lbp, int nbins, int64_t cells) {
+    const int pitch = round_up(cols, 16);
+    const int unit = cell_rows ? cell_rows : 16;
+    const int B = std::max(unit, int(chunk_bytes() / size_t(pitch)) / unit * unit);
+    const int n_bands = (rows + B - 1) / B;
+    const int grid_c = cell_rows ? cols / cell_cols : 1;
+    const size_t band_hist = cell_rows ? size_t(B / cell_rows) * grid_c * nbins : size_t(nbins);
+    const bool stage_px = !is_pinned(px);
+    const bool stage_codes = codes && !is_pinned(codes);
+    std::vector<uint32_t> whole(hist32 && !cell_rows ? size_t(n_bands) * nbins : 0);
+    aldp_status s = ALDP_OK;
+    const int used = std::min(n_bands, kSlots);
+    for (int i = 0; i < used; ++i) {
+        Slot& sl = c.slot[i];
+        s = ensure(reinterpret_cast<void**>(&sl.d_px), &sl.px_cap, size_t(B + 2) * pitch);
+        if (s == ALDP_OK && codes) s = ensure(reinterpret_cast<void**>(&sl.d_codes), &sl.codes_cap, size_t(B) * pitch);
+        if (s == ALDP_OK && hist32)
+            s = ensure(reinterpret_cast<void**>(&sl.d_hist), &sl.hist_cap, sizeof(uint32_t) * band_hist);
+        if (s == ALDP_OK && stage_px) s = ensure_pinned(sl.h_px, size_t(B + 2) * pitch);
+        if (s == ALDP_OK && stage_codes) s = ensure_pinned(sl.h_codes, size_t(B) * pitch);
+        if (s == ALDP_OK && hist32) s = ensure_pinned(sl.h_hist, sizeof(uint32_t) * band_hist);
+        if (s != ALDP_OK) return s;
+    }
+    int pending[kSlots];
+    for (int i = 0; i < kSlots; ++i) pending[i] = -1;
+    auto band_rows = [&](int b, int& start, int& end) {
+        start = b * B;
+        end = std::min(rows, start + B);
+    };
+    auto drain = [&](int si) -> aldp_status {
+        const int b = pending[si];
+        if (b < 0) return ALDP_OK;
+        Slot& sl = c.slot[si];
+        HOST_CUDA_TRY(cudaEventSynchronize(sl.done));
+        int start, end;
+        band_rows(b, start, end);
+        if (stage_codes)
+            copy_rows(codes + size_t(start) * cols, cols, static_cast<const uint8_t*>(sl.h_codes.p), pitch, cols,
+                      size_t(end - start));
+        if (hist32 && (!cell_rows || end - start >= cell_rows)) {
+            const uint32_t* h = static_cast<const uint32_t*>(sl.h_hist.p);
+            if (cell_rows) {
+                const size_t n_cell_rows = size_t(std::min(end, rows / cell_rows * cell_rows) - start) / cell_rows;
+                std::memcpy(hist32 + size_t(start / cell_rows) * grid_c * nbins, h,
+                            sizeof(uint32_t) * n_cell_rows * grid_c * nbins);
+            } else {
+                std::memcpy(whole.data() + size_t(b) * nbins, h, sizeof(uint32_t) * nbins);
+            }
+        }
+        pending[si] = -1;
+        return ALDP_OK;
+    };
+    for (int b = 0; b < n_bands; ++b) {
+        const int si = b % kSlots;
+        Slot& sl = c.slot[si];
+        const cudaStream_t st = sl.stream;
+        s = drain(si);
+        if (s != ALDP_OK) return s;
+        int start, end;
+        band_rows(b, start, end);
+        const int top = start > 0 ? 1 : 0, bot = end < rows ? 1 : 0;
+        const int src_rows = end - start + top + bot;
+        if (stage_px) {
+            copy_rows(static_cast<uint8_t*>(sl.h_px.p), pitch, px + size_t(start - top) * cols, cols, cols,
+                      size_t(src_rows));
+            HOST_CUDA_TRY(cudaMemcpyAsync(sl.d_px, sl.h_px.p, size_t(src_rows) * pitch, cudaMemcpyHostToDevice, st));
+        } else {
+            HOST_CUDA_TRY(cudaMemcpy2DAsync(sl.d_px, pitch, px + size_t(start - top) * cols, cols, cols,
+                                            size_t(src_rows), cudaMemcpyHostToDevice, st));
+        }
+        aldp_ldp_args a{};
+        a.d_pixels = sl.d_px + size_t(top) * pitch;
+        a.img_stride = int64_t(B + 2) * pitch;
+        a.rows = end - start;
+        a.cols = cols;
+        a.pitch = pitch;
+        a.n_images = 1;
+        a.k = k;
+        // a band shorter than a cell (the frame's remainder rows) has no cells
+        const bool band_cells = cell_rows && a.rows >= cell_rows;
+        a.cell_rows = band_cells ? cell_rows : 0;
+        a.cell_cols = band_cells ? cell_cols : 0;
+        a.d_codes = codes ? sl.d_codes : nullptr;
+        a.codes_img_stride = int64_t(B) * pitch;
+        a.codes_pitch = pitch;
+        a.d_hist = hist32 && (band_cells || !cell_rows) ? sl.d_hist : nullptr;
+        a.rows_above = top;
+        a.rows_below = bot;
+        if (a.d_codes || a.d_hist) {
+            s = lbp ? aldp_lbp_batch(&a, st) : aldp_ldp_batch(&a, st);
+            if (s != ALDP_OK) return hfail(s, aldp_last_error());
+        }
+        if (codes) {
+            if (stage_codes)
+                HOST_CUDA_TRY(cudaMemcpyAsync(sl.h_codes.p, sl.d_codes, size_t(a.rows) * pitch, cudaMemcpyDeviceToHost, st));
+            else
+                HOST_CUDA_TRY(cudaMemcpy2DAsync(codes + size_t(start) * cols, cols, sl.d_codes, pitch, cols,
+                                                size_t(a.rows), cudaMemcpyDeviceToHost, st));
+        }
+        if (a.d_hist)
+            HOST_CUDA_TRY(cudaMemcpyAsync(sl.h_hist.p, sl.d_hist,
+                                          sizeof(uint32_t) * (band_cells ? size_t(a.rows / cell_rows) * grid_c * nbins
+                                                                         : size_t(nbins)),
+                                          cudaMemcpyDeviceToHost, st));
+        HOST_CUDA_TRY(cudaEventRecord(sl.done, st));
+        pending[si] = b;  // drained (and its staging freed) before the slot's next band
+    }
+    for (int i = 0; i < used; ++i) {
+        s = drain(i);
+        if (s != ALDP_OK) return s;
+    }
+    for (int i = 0; i < used; ++i) HOST_CUDA_TRY(cudaStreamSynchronize(c.slot[i].stream));
+    if (hist32 && !cell_rows) {
+        for (int bin = 0; bin < nbins; ++bin) {
+            uint32_t t = 0;
+            for (int b = 0; b < n_bands; ++b) t += whole[size_t(b) * nbins + bin];
+            hist32[bin] = t;
+        }
+    }
+    (void)cells;
+    return ALDP_OK;
+}
+
 // Shared body: host pixels (n contiguous rows x cols images) -> optional host
 // codes (contiguous) and u32 histograms `hist32` [n][cells][bins]. Pinned
 // host memory gives full PCIe rate in both directions at once.
@@ -184,7 +324,7 @@ static aldp_status host_batch(const uint8_t* px, int n, int rows, int cols, int 
     const size_t img_bytes = size_t(pitch) * rows;
     const size_t plane = size_t(rows) * cols;
     const size_t hist_per_img = size_t(cells) * nbins;
-    const int chunk = int(std::max<size_t>(1, std::min<size_t>(size_t(n), kChunkBytes / img_bytes)));
+    const int chunk = int(std::max<size_t>(1, std::min<size_t>(size_t(n), chunk_bytes() / img_bytes)));
     const int n_chunks = (n + chunk - 1) / chunk;
     const int used = std::min(n_chunks, kSlots);
     // Small calls (the reference's one-image-per-call pattern): stage through
@@ -241,6 +381,11 @@ static aldp_status host_batch(const uint8_t* px, int n, int rows, int cols, int 
         if (hist32) std::memcpy(hist32, c.h_hist.p, sizeof(uint32_t) * hist_per_img * n);
         return ALDP_OK;
     }
+    // One frame taller than a chunk: stream it as bands of whole cells (or
+    // of 16-row multiples), each with its real neighbour rows as halos, so
+    // H2D, kernel and D2H overlap inside the frame too.
+    if (n == 1 && !user && img_bytes > chunk_bytes()) return host_band(c, px, rows, cols, k, cell_rows, cell_cols,
+                                                                       codes, hist32, lbp, nbins, cells);
     // order the internal streams after work already queued on the caller's stream
     cudaEvent_t start = nullptr;
     if (user) {

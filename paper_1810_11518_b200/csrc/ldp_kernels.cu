@@ -68,6 +68,7 @@ struct GenericParams {
     int nbins;
     int cell_rows, cell_cols, grid_r, grid_c;  // cell_rows == 0: whole image
     int cell_clamp;                            // 0: cells cut from the whole-image code map
+    int row_lo, row_hi;                        // neighbour rows readable (halo rows of a band view)
 };
 
 __global__ void ldp_generic_kernel(GenericParams p) {
@@ -80,8 +81,8 @@ __global__ void ldp_generic_kernel(GenericParams p) {
         const int x = int(rem / p.cols), y = int(rem - int64_t(x) * p.cols);
         const uint8_t* base = p.px + img * p.img_stride;
         // k == 0: LBP (256 bins indexed by the code itself)
-        const unsigned code = p.k ? clamped_code(base, p.pitch, x, y, 0, p.rows - 1, 0, p.cols - 1, p.k)
-                                  : clamped_lbp(base, p.pitch, x, y, 0, p.rows - 1, 0, p.cols - 1);
+        const unsigned code = p.k ? clamped_code(base, p.pitch, x, y, p.row_lo, p.row_hi, 0, p.cols - 1, p.k)
+                                  : clamped_lbp(base, p.pitch, x, y, p.row_lo, p.row_hi, 0, p.cols - 1);
         if (p.codes)
             p.codes[img * p.codes_img_stride + int64_t(x) * p.codes_pitch + y] = uint8_t(code);
         if (!p.hist) continue;
@@ -279,6 +280,8 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
         p.cell_rows = a->cell_rows;
         p.cell_cols = a->cell_cols;
         p.cell_clamp = a->cell_from_map ? 0 : 1;
+        p.row_lo = a->rows_above ? -1 : 0;
+        p.row_hi = a->rows - 1 + (a->rows_below ? 1 : 0);
         p.edge_lo = p.cell_clamp ? 0 : -1;
         p.edge_hi = p.cell_clamp ? a->cell_rows - 1 : -1;
         p.grid_r = grid_r;
@@ -321,6 +324,8 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
     g.cell_rows = a->cell_rows;
     g.cell_cols = a->cell_cols;
     g.cell_clamp = a->cell_from_map ? 0 : 1;
+    g.row_lo = a->rows_above ? -1 : 0;
+    g.row_hi = a->rows - 1 + (a->rows_below ? 1 : 0);
     g.grid_r = grid_r;
     g.grid_c = grid_c;
     const int64_t total = int64_t(a->rows) * a->cols * a->n_images;

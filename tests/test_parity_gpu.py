@@ -447,3 +447,69 @@ def test_fast_kernel_any_width(cols):
     torch.cuda.synchronize()
     if pitch > cols:
         assert bool((codes[:, :, cols:] == 0xAB).all())
+
+
+@pytest.mark.parametrize("kernel", ["auto", "generic"])
+def test_band_views_with_halo_rows(kernel):
+    """A tall frame processed as bands (views into the resident frame with
+    halo=(1, 1) on inner edges) gives the frame's exact codes and histograms:
+    whole-image histograms sum, cell grids tile (bands of whole cells)."""
+    r, c = 300, 200
+    img = oracle.make_random(r, c, 4242)
+    d = to_dev(img)
+    pitch = d.shape[2]
+    want_c, want_w = oracle.batch(img, k=3)
+    _, want_cells = oracle.batch(img, k=3, cell=(20, 25), codes=False)
+    for B in (40, 60, 100):  # multiples of the 20-row cells
+        codes = np.zeros((r, c), np.uint8)
+        whole = np.zeros(56, np.uint64)
+        cells = []
+        for s0 in range(0, r, B):
+            s1 = min(r, s0 + B)
+            view = d[:, s0:s1, :]
+            cb, hb = aldp.ldp_batch(view, s1 - s0, c, k=3, codes=True, hist=True, kernel=kernel,
+                                    halo=(s0 > 0, s1 < r))
+            _, hc = aldp.ldp_batch(view, s1 - s0, c, k=3, cell=(20, 25), hist=True, kernel=kernel,
+                                   halo=(s0 > 0, s1 < r))
+            torch.cuda.synchronize()
+            codes[s0:s1] = cb[0, :, :c].cpu().numpy()
+            whole += hb[0, 0].cpu().numpy().astype(np.uint64)
+            cells.append(hc[0].cpu().numpy().astype(np.uint64))
+        assert np.array_equal(codes, want_c[0]), (B, kernel)
+        assert np.array_equal(whole, want_w[0, 0]), (B, kernel)
+        assert np.array_equal(np.concatenate(cells), want_cells[0]), (B, kernel)
+    assert pitch >= c
+
+
+def test_host_banded_tall_frames():
+    """Single frames taller than a host chunk stream as bands with halo rows
+    (ALDP_CHUNK_BYTES shrinks the chunk so small frames take that path), for
+    pageable and pinned buffers, whole-image and cell histograms, LDP and LBP."""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import json, sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1810_11518_b200 as aldp, oracle
+out = []
+for (r, c, cell, k) in [(333, 250, (0, 0), 3), (333, 250, (20, 25), 3), (517, 96, (32, 32), 5),
+                        (333, 250, (0, 0), 0), (333, 250, (21, 25), 0), (64, 4000, (9, 40), 3)]:
+    img = oracle.make_random(r, c, r * c + k)
+    want_c, want_h = oracle.batch(img, k=k, cell=cell)
+    for pinned in (False, True):
+        src = img[None].copy()
+        if pinned:
+            t = torch.from_numpy(src).pin_memory()
+            src = t.numpy()
+        codes, hist = aldp.ldp_batch_host(src, k=k, cell=cell)
+        out.append(bool(np.array_equal(codes, want_c) and np.array_equal(hist.astype(np.uint64), want_h)))
+print(json.dumps(out))
+'''
+    env = dict(os.environ, ALDP_CHUNK_BYTES="20000")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code, root], capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    assert all(res), res
