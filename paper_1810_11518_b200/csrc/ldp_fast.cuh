@@ -220,7 +220,10 @@ __device__ __forceinline__ void load_words(const uint8_t* p, uint32_t (&w)[NW]) 
 }
 
 // K = 1..7 (not 4): LDP with top-K codes; K = 0: LBP (descriptors.cpp:141-168).
-template <int K, int NW, bool CELLS, bool CODES, bool HIST>
+// HALO: the view is a band of a taller resident frame (rows -1 / rows are
+// real neighbours); a separate instantiation keeps the common path's row
+// clamp a compile-time [0, rows) (a runtime bound measured 1.8 % slower).
+template <int K, int NW, bool CELLS, bool CODES, bool HIST, bool HALO = false>
 __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_kernel(FastParams p) {
     constexpr bool LBP = K == 0;
     constexpr int REGION = LBP ? 1024 : kRegion;  // LBP: 256 counts; LDP: code table + 64 counts
@@ -364,7 +367,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
         const uint8_t* const halo_p = img_px + halo_off;
         const uint8_t* const pf_p = img_px + c0;
         auto load_raw = [&](int r) -> RawN<NW> {
-            const int rr = min(max(r, p.row_lo), p.row_hi);
+            const int rr = HALO ? min(max(r, p.row_lo), p.row_hi) : min(max(r, 0), p.rows - 1);
             if (!CELLS && sl == 1) {  // pull a row further ahead into L2 (measured: pays only without cells)
                 const int ra_ = min(r + kL2Ahead, p.rows - 1);
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(pf_p + (long long)ra_ * p.pitch));

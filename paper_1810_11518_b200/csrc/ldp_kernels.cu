@@ -127,9 +127,9 @@ static int n_sms() {
     return cache[dev];
 }
 
-template <int K, int NW, bool CELLS, bool CODES, bool HIST>
+template <int K, int NW, bool CELLS, bool CODES, bool HIST, bool HALO>
 static aldp_status launch_fast_t(const FastParams& p, cudaStream_t st) {
-    auto kern = ldp_fast_kernel<K, NW, CELLS, CODES, HIST>;
+    auto kern = ldp_fast_kernel<K, NW, CELLS, CODES, HIST, HALO>;
     constexpr int NSEG = 32 / (kTileCols / (4 * NW));
     constexpr int REGION = K == 0 ? 1024 : kRegion;  // LBP: 256 counts per region
     const size_t smem = size_t(kFastWarps) * NSEG * kSegRegions * REGION + REGION;  // + alignment slack
@@ -160,44 +160,38 @@ static aldp_status launch_fast_t(const FastParams& p, cudaStream_t st) {
     return ALDP_OK;
 }
 
-template <int K, int NW>
+template <int K, int NW, bool HALO>
 static aldp_status launch_fast_kw(const FastParams& p, bool cells, cudaStream_t st) {
     const bool codes = p.codes != nullptr, hist = p.hist != nullptr;
     if (cells) {  // cell geometry only matters for histograms
-        return codes ? launch_fast_t<K, NW, true, true, true>(p, st)
-                     : launch_fast_t<K, NW, true, false, true>(p, st);
+        return codes ? launch_fast_t<K, NW, true, true, true, HALO>(p, st)
+                     : launch_fast_t<K, NW, true, false, true, HALO>(p, st);
     }
-    if (codes && hist) return launch_fast_t<K, NW, false, true, true>(p, st);
-    if (codes) return launch_fast_t<K, NW, false, true, false>(p, st);
-    return launch_fast_t<K, NW, false, false, true>(p, st);
+    if (codes && hist) return launch_fast_t<K, NW, false, true, true, HALO>(p, st);
+    if (codes) return launch_fast_t<K, NW, false, true, false, HALO>(p, st);
+    return launch_fast_t<K, NW, false, false, true, HALO>(p, st);
 }
+
+// Two 4-byte words per lane (NW = 2; one word per lane measured slower).
+constexpr int kLaneWords = 2;
 
 template <int K>
-static aldp_status launch_fast_k(const FastParams& p, bool cells, int nw, cudaStream_t st) {
-    return nw == 2 ? launch_fast_kw<K, 2>(p, cells, st) : launch_fast_kw<K, 1>(p, cells, st);
+static aldp_status launch_fast_k(const FastParams& p, bool cells, bool halo, cudaStream_t st) {
+    return halo ? launch_fast_kw<K, kLaneWords, true>(p, cells, st)
+                : launch_fast_kw<K, kLaneWords, false>(p, cells, st);
 }
 
-static aldp_status launch_fast(const FastParams& p, int k, bool cells, int nw, cudaStream_t st) {
+static aldp_status launch_fast(const FastParams& p, int k, bool cells, bool halo, cudaStream_t st) {
     switch (k) {
-    case 0: return launch_fast_k<0>(p, cells, nw, st);  // LBP
-    case 1: return launch_fast_k<1>(p, cells, nw, st);
-    case 2: return launch_fast_k<2>(p, cells, nw, st);
-    case 3: return launch_fast_k<3>(p, cells, nw, st);
-    case 5: return launch_fast_k<5>(p, cells, nw, st);
-    case 6: return launch_fast_k<6>(p, cells, nw, st);
-    case 7: return launch_fast_k<7>(p, cells, nw, st);
+    case 0: return launch_fast_k<0>(p, cells, halo, st);  // LBP
+    case 1: return launch_fast_k<1>(p, cells, halo, st);
+    case 2: return launch_fast_k<2>(p, cells, halo, st);
+    case 3: return launch_fast_k<3>(p, cells, halo, st);
+    case 5: return launch_fast_k<5>(p, cells, halo, st);
+    case 6: return launch_fast_k<6>(p, cells, halo, st);
+    case 7: return launch_fast_k<7>(p, cells, halo, st);
     default: return fail(ALDP_EINVAL, "fast kernel: unsupported k");
     }
-}
-
-// Words (4-byte column groups) per lane of the fast kernel: 2 (default) or 1.
-// ALDP_LANE_WORDS overrides it for experiments.
-static int lane_words() {
-    static const int nw = [] {
-        const char* e = std::getenv("ALDP_LANE_WORDS");
-        return (e && std::atoi(e) == 1) ? 1 : 2;
-    }();
-    return nw;
 }
 
 // Most cells a 128-column tile can touch for this geometry.
@@ -251,8 +245,7 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
                                       sizeof(uint32_t) * size_t(a->n_images) * cells * nbins, st));
     if (a->n_images == 0 || (!a->d_codes && !a->d_hist)) return ALDP_OK;
 
-    const int nw = lane_words();
-    const int al = 4 * nw;  // alignment the per-lane vector loads/stores need
+    const int al = 4 * kLaneWords;  // alignment the per-lane vector loads/stores need
     const bool aligned =
         a->pitch % al == 0 && (a->n_images <= 1 || a->img_stride % al == 0) &&
         (reinterpret_cast<uintptr_t>(a->d_pixels) % al) == 0 &&
@@ -306,7 +299,7 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
                 p.id_code[tag_xor(c)] = uint8_t(c);
                 p.id_bin[tag_xor(c)] = uint8_t(colex_rank(c));
             }
-        return launch_fast(p, k, a->cell_rows != 0 && a->d_hist != nullptr, nw, st);
+        return launch_fast(p, k, a->cell_rows != 0 && a->d_hist != nullptr, a->rows_above || a->rows_below, st);
     }
     GenericParams g{};
     g.px = a->d_pixels;
