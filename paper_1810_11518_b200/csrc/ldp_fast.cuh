@@ -4,9 +4,9 @@
 // row) x 128 columns. A tile is processed by a segment of 128/(4*NW) lanes;
 // each lane owns NW 4-byte words (4*NW adjacent columns) and slides down the
 // band with three unpacked rows in registers and three raw rows in flight
-// (software prefetch, distance 3) plus an L2 prefetch further ahead. NW = 1
-// (32-lane segments, one tile per warp, light registers -> high occupancy)
-// or NW = 2 (16-lane segments, two tiles per warp).
+// (software prefetch, distance 3) plus an L2 prefetch further ahead. The
+// library instantiates NW = 2 (16-lane segments, two tiles per warp); NW = 1
+// (32-lane segments, one tile per warp) compiles but measured slower.
 //
 // Per lane and row, each word becomes two u16x2 pixel pairs with stride-2
 // packing: word j (columns y+4j .. y+4j+3) gives A = (y+4j, y+4j+2) and
