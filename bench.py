@@ -174,6 +174,8 @@ def run_reference(args, cfg_name):
     if rank != 0:
         return 0
     n, rows, cols, k, cr, cc, blobs, gen, seed = CONFIGS[cfg_name]
+    if args.k >= 0:
+        k = args.k
     threads = os.cpu_count() or 1
     sample = max(threads * 4, 32) if cfg_name in ("c5", "c2", "c5w", "c5lbp") else \
         (threads if cfg_name == "c3" else 1)
@@ -279,6 +281,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
     ap.add_argument("--images", type=int, default=0, help="override batch size (testing)")
+    ap.add_argument("--k", type=int, default=-1, help="override the config's k (C3 sweeps 1, 3, 5)")
     ap.add_argument("--e2e-images", type=int, default=2048)
     ap.add_argument("--cpu-images", type=int, default=0, help="0 = auto (~10-30 s of CPU work)")
     ap.add_argument("--no-cpu", action="store_true")
@@ -318,6 +321,8 @@ def main():
     n, rows, cols, k, cr, cc, blobs, gen, seed = CONFIGS[args.config]
     if args.images:
         n = args.images
+    if args.k >= 0:
+        k = args.k
     lo, hi = shard_range(n, rank, world)
     mine = hi - lo
     pitch = cols  # 640/1024/16384: already 16-byte aligned
