@@ -145,6 +145,24 @@ __device__ __forceinline__ uint32_t topk_from_pairs(uint32_t pA, uint32_t qA, ui
     }
 }
 
+// k == 4: 70 four-subsets do not fit the 6-bit XOR id, but the tag set keeps
+// (XOR of the subset's tags, whether direction 0 is in it) unique (checked on
+// the host). Both halves are sorted fully, the bitonic half-cleaner keeps the
+// top four {max(a1,b4), max(a2,b3), max(a3,b2), max(a4,b1)}, and bit 6 of
+// each lane's id is set when K0 >= the fourth largest. ~33 ops per pair.
+__device__ __forceinline__ uint32_t top4_id(uint32_t pA, uint32_t qA, uint32_t rA, uint32_t sA, uint32_t pB,
+                                            uint32_t qB, uint32_t rB, uint32_t sB, uint32_t k0) {
+    const uint32_t a1 = vmax(pA, rA), a4 = vmin(qA, sA), xA = vmin(pA, rA), yA = vmax(qA, sA);
+    const uint32_t a2 = vmax(xA, yA), a3 = vmin(xA, yA);
+    const uint32_t b1 = vmax(pB, rB), b4 = vmin(qB, sB), xB = vmin(pB, rB), yB = vmax(qB, sB);
+    const uint32_t b2 = vmax(xB, yB), b3 = vmin(xB, yB);
+    const uint32_t c1 = vmax(a1, b4), c2 = vmax(a2, b3), c3 = vmax(a3, b2), c4 = vmax(a4, b1);
+    const uint32_t t4 = vmin(vmin3(c1, c2, c3), c4);
+    // lane of e is 0 iff K0 >= t4 (keys unique): min(e, 1) ^ 1 is the flag
+    const uint32_t in0 = (vmin(vmax(k0, t4) ^ k0, 0x00010001u) ^ 0x00010001u) << 6;
+    return ((c1 ^ c2 ^ c3 ^ c4) & 0xFFBFFFBFu) | in0;
+}
+
 template <int K>
 __device__ __forceinline__ uint32_t topk_id(const uint32_t (&k)[8]) {
     return topk_from_pairs<K>(vmax(k[0], k[1]), vmin(k[0], k[1]), vmax(k[2], k[3]), vmin(k[2], k[3]),

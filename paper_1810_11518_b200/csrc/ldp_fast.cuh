@@ -66,8 +66,8 @@ struct FastParams {
     int band_rows, bands, blocks;
     int64_t n_tiles;
     uint32_t one;         // 1 at run time: multiplier that keeps integer adds on the FMA pipe
-    uint8_t id_code[64];  // XOR id -> code (0 where no code has that id)
-    uint8_t id_bin[64];   // XOR id -> histogram bin (colex rank of the code)
+    uint8_t id_code[128];  // id -> code (0 where no code has that id); 7-bit ids for k == 4
+    uint8_t id_bin[128];   // id -> histogram bin (colex rank of the code)
 };
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
@@ -113,9 +113,14 @@ __device__ __forceinline__ uint32_t pair_id(const Col& a, const Col& b, const Co
         const uint32_t k5 = c.lc + b.l + T5, k7 = c.cr + b.r + T7;
         const uint32_t x0 = a.r + b.r + T0, x4 = a.l + b.l + T4;   // + c.r / + c.l fused
         const uint32_t x2 = a.lc + T2, x6 = c.lc + T6;             // + a.r / + c.r fused
-        return topk_from_pairs<K>(vaddmax(x0, c.r, k1), vaddmin(x0, c.r, k1), vaddmax(x2, a.r, k3),
-                                  vaddmin(x2, a.r, k3), vaddmax(x4, c.l, k5), vaddmin(x4, c.l, k5),
-                                  vaddmax(x6, c.r, k7), vaddmin(x6, c.r, k7));
+        if constexpr (K == 4)
+            return top4_id(vaddmax(x0, c.r, k1), vaddmin(x0, c.r, k1), vaddmax(x2, a.r, k3), vaddmin(x2, a.r, k3),
+                           vaddmax(x4, c.l, k5), vaddmin(x4, c.l, k5), vaddmax(x6, c.r, k7), vaddmin(x6, c.r, k7),
+                           fadd(x0, c.r, one));
+        else
+            return topk_from_pairs<K>(vaddmax(x0, c.r, k1), vaddmin(x0, c.r, k1), vaddmax(x2, a.r, k3),
+                                      vaddmin(x2, a.r, k3), vaddmax(x4, c.l, k5), vaddmin(x4, c.l, k5),
+                                      vaddmax(x6, c.r, k7), vaddmin(x6, c.r, k7));
     } else {
     const uint32_t k0 = fadd(fadd(a.r, b.r, one), c.r, one) + T0;  // TR + R + BR
     const uint32_t k4 = fadd(fadd(a.l, b.l, one), c.l, one) + T4;  // BL + L + TL
@@ -226,9 +231,10 @@ __device__ __forceinline__ void load_words(const uint8_t* p, uint32_t (&w)[NW]) 
 template <int K, int NW, bool CELLS, bool CODES, bool HIST, bool HALO = false>
 __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_kernel(FastParams p) {
     constexpr bool LBP = K == 0;
-    constexpr int REGION = LBP ? 1024 : kRegion;  // LBP: 256 counts; LDP: code table + 64 counts
-    constexpr int CNT = LBP ? 0 : 256;             // offset of the counts in a region
-    constexpr int NT = LBP ? 256 : 64;             // table entries (codes / XOR ids)
+    // LBP: 256 counts; LDP: code table + 64 counts; k == 4: code table + 128 counts
+    constexpr int REGION = (LBP || K == 4) ? 1024 : kRegion;
+    constexpr int CNT = LBP ? 0 : (K == 4 ? 512 : 256);  // offset of the counts in a region
+    constexpr int NT = LBP ? 256 : (K == 4 ? 128 : 64);  // table entries (codes / ids)
     constexpr int SEG_SMEM = kSegRegions * REGION;
     constexpr int LC = 4 * NW;              // columns per lane
     constexpr int SEG = kTileCols / LC;     // lanes per segment (tile)
@@ -240,7 +246,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
 #endif
     constexpr int SUMS = CELLS ? ALDP_CELL_SUMS : 2;  // measured: all stored sums win only without cells
     extern __shared__ __align__(512) uint8_t smem[];
-    __shared__ uint8_t id_bin[64];
+    __shared__ uint8_t id_bin[128];
     __shared__ int fix_cols[kFastWarps][NSEG][kFixList];
     __shared__ int fix_n[kFastWarps][NSEG];
 
@@ -260,9 +266,9 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
         const int words = kFastWarps * NSEG * SEG_SMEM / 4;
         for (int i = threadIdx.x; i < words; i += blockDim.x) {
             const int in_region = i & (REGION / 4 - 1);
-            w[i] = (!LBP && in_region < 64) ? uint32_t(p.id_code[in_region]) : 0u;
+            w[i] = (!LBP && in_region < NT) ? uint32_t(p.id_code[in_region]) : 0u;
         }
-        if (!LBP && threadIdx.x < 64) id_bin[threadIdx.x] = p.id_bin[threadIdx.x];
+        if (!LBP && threadIdx.x < NT) id_bin[threadIdx.x] = p.id_bin[threadIdx.x];
     }
     __syncthreads();
 
@@ -483,7 +489,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
                 } else {
                     uint32_t e[LC];
 #pragma unroll
-                    for (int s = 0; s < LC; ++s) e[s] = lds32(ad[s] - 256);
+                    for (int s = 0; s < LC; ++s) e[s] = lds32(ad[s] - CNT);
 #pragma unroll
                     for (int j = 0; j < NW; ++j)  // bytes -> word with multiply-adds (FMA pipe)
                         wd[j] = e[4 * j] + e[4 * j + 1] * 0x100u + e[4 * j + 2] * 0x10000u + e[4 * j + 3] * 0x1000000u;

@@ -131,7 +131,7 @@ template <int K, int NW, bool CELLS, bool CODES, bool HIST, bool HALO>
 static aldp_status launch_fast_t(const FastParams& p, cudaStream_t st) {
     auto kern = ldp_fast_kernel<K, NW, CELLS, CODES, HIST, HALO>;
     constexpr int NSEG = 32 / (kTileCols / (4 * NW));
-    constexpr int REGION = K == 0 ? 1024 : kRegion;  // LBP: 256 counts per region
+    constexpr int REGION = (K == 0 || K == 4) ? 1024 : kRegion;  // LBP: 256 counts, k == 4: 7-bit ids
     const size_t smem = size_t(kFastWarps) * NSEG * kSegRegions * REGION + REGION;  // + alignment slack
     // The shared-memory opt-in is a per-device function attribute: set it once
     // per device this process launches on (several GPUs in one process work).
@@ -187,6 +187,7 @@ static aldp_status launch_fast(const FastParams& p, int k, bool cells, bool halo
     case 1: return launch_fast_k<1>(p, cells, halo, st);
     case 2: return launch_fast_k<2>(p, cells, halo, st);
     case 3: return launch_fast_k<3>(p, cells, halo, st);
+    case 4: return launch_fast_k<4>(p, cells, halo, st);
     case 5: return launch_fast_k<5>(p, cells, halo, st);
     case 6: return launch_fast_k<6>(p, cells, halo, st);
     case 7: return launch_fast_k<7>(p, cells, halo, st);
@@ -253,10 +254,10 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
                          (a->n_images <= 1 || a->codes_img_stride % al == 0)));
     int ncl = 1;
     if (a->cell_rows) ncl = max_cells_per_tile(a->cols, a->cell_cols, grid_c);
-    const bool fast_ok = aligned && k != 4 && ncl <= kMaxTileCells;
+    const bool fast_ok = aligned && ncl <= kMaxTileCells;
     if (kernel == ALDP_KERNEL_FAST && !fast_ok)
-        return fail(ALDP_EINVAL, "fast kernel needs 8-byte aligned pitches/strides, "
-                                 "k != 4 and at most 5 cells per 128 columns");
+        return fail(ALDP_EINVAL, "fast kernel needs 8-byte aligned pitches/strides "
+                                 "and at most 5 cells per 128 columns");
     if (kernel != ALDP_KERNEL_GENERIC && fast_ok) {
         FastParams p{};
         p.px = a->d_pixels;
@@ -293,11 +294,14 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
         p.bands = (a->rows + p.band_rows - 1) / p.band_rows;
         p.n_tiles = int64_t(a->n_images) * p.bands * p.blocks;
         p.one = 1;
-        for (int id = 0; id < 64; ++id) p.id_code[id] = p.id_bin[id] = 0;
+        for (int id = 0; id < 128; ++id) p.id_code[id] = p.id_bin[id] = 0;
         for (int c = 0; c < 256 && k; ++c)
             if (popcount8(c) == k) {
-                p.id_code[tag_xor(c)] = uint8_t(c);
-                p.id_bin[tag_xor(c)] = uint8_t(colex_rank(c));
+                // k == 4: the 6-bit XOR plus "direction 0 selected" (ldp_common.cuh top4_id)
+                const int id = int(tag_xor(c)) | (k == 4 ? (c & 1) << 6 : 0);
+                if (p.id_code[id]) return fail(ALDP_EINVAL, "internal: code id collision");
+                p.id_code[id] = uint8_t(c);
+                p.id_bin[id] = uint8_t(colex_rank(c));
             }
         return launch_fast(p, k, a->cell_rows != 0 && a->d_hist != nullptr, a->rows_above || a->rows_below, st);
     }

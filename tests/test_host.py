@@ -88,6 +88,9 @@ def test_tag_set_properties():
     for k in (1, 2, 3, 5, 6, 7):
         ids = [reduce(lambda a, b: a ^ b, (TAGS[i] for i in s)) for s in itertools.combinations(range(8), k)]
         assert len(set(ids)) == len(ids), k
+    # k == 4: the XOR plus "direction 0 selected" is unique (7-bit id, top4_id)
+    ids4 = [(reduce(lambda a, b: a ^ b, (TAGS[i] for i in s)), 0 in s) for s in itertools.combinations(range(8), 4)]
+    assert len(set(ids4)) == 70
 
 
 def test_key_order_is_reference_order():

@@ -95,7 +95,7 @@ def test_random_images_every_k(k):
             assert np.array_equal(h, want_h), (shape, k, kern)
 
 
-@pytest.mark.parametrize("k", [1, 2, 3, 5, 6, 7])
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 6, 7])
 def test_tie_heavy_every_k(k):
     """Values {0,1,2} with constant rectangles (config-3 style)."""
     px = aldp.gen_ties(6, 64, 128, seed=7 + k, device=DEV)
@@ -125,7 +125,7 @@ def test_cell_histograms_k_sweep():
     px = aldp.gen_faces(2, 162, 184, blobs=8, seed=3, device=DEV)
     torch.cuda.synchronize()
     host = px[:, :, :184].cpu().numpy()
-    for k in (1, 2, 3, 5, 6, 7):
+    for k in (1, 2, 3, 4, 5, 6, 7):
         want_c, want_h = oracle.batch(host, k=k, cell=(81, 91))
         c, h = run(host, k, cell=(81, 91), kernel="fast")
         assert np.array_equal(c, want_c), k
@@ -248,9 +248,9 @@ def test_host_entry_point_errors():
         aldp.windowed_features(img, 11)               # window > image
     with pytest.raises(ValueError):
         aldp.ldp_code_map(img, 8)                     # k out of [1, 7]
-    px = to_dev(img)
+    px = to_dev(img, pitch=10)  # pitch not 8-byte aligned: the packed kernel refuses
     with pytest.raises(ValueError):
-        aldp.ldp_batch(px, 10, 10, k=4, cell=(5, 5), codes=True, hist=True, kernel="fast")
+        aldp.ldp_batch(px, 10, 10, k=3, cell=(5, 5), codes=True, hist=True, kernel="fast")
 
 
 def test_empty_batch_and_constant_images():
