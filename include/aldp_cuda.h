@@ -96,7 +96,7 @@ aldp_status aldp_ldp_batch(const aldp_ldp_args* args, void* stream);
 
 /* Kernel selection for aldp_ldp_batch: AUTO picks the packed sm_100a kernel
  * whenever the layout allows it (pitches, strides and base pointers 8-byte
- * aligned -- any width -- k != 4, at most 5 cells per 128 columns) and the
+ * aligned -- any width and any k -- at most 5 cells per 128 columns) and the
  * generic per-pixel kernel otherwise. FAST fails with
  * ALDP_EINVAL when the layout does not allow it. Both are CUDA; there is no
  * CPU path. */

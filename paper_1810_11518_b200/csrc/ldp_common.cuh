@@ -115,7 +115,7 @@ __device__ __forceinline__ uint32_t vaddmin(uint32_t a, uint32_t b, uint32_t c) 
 template <int K>
 __device__ __forceinline__ uint32_t topk_from_pairs(uint32_t pA, uint32_t qA, uint32_t rA, uint32_t sA,
                                                     uint32_t pB, uint32_t qB, uint32_t rB, uint32_t sB) {
-    static_assert(K >= 1 && K <= 7 && K != 4, "k == 4 uses the generic kernel");
+    static_assert(K >= 1 && K <= 7 && K != 4, "k == 4 selects through top4_id");
     if constexpr (K == 1) {
         return vmax(vmax3(pA, rA, pB), rB);
     } else if constexpr (K == 7) {  // complement of the single smallest key

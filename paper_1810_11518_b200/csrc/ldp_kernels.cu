@@ -9,9 +9,9 @@
 //    an 18-op min/max top-k network per pair, a 6-bit XOR id, one shared-
 //    memory table lookup per pixel for the code, one per-lane shared-memory
 //    atomic per pixel for the histogram, one coalesced 4-byte code store.
-//  * ldp_generic_kernel -- one thread per pixel, any geometry and any k
-//    (including k == 4, which the XOR id cannot name). Used for layouts the
-//    fast kernel does not take (odd widths/pitches) and tiny images.
+//  * ldp_generic_kernel -- one thread per pixel, any geometry and any k.
+//    Used for layouts the fast kernel does not take (pitches, strides or
+//    base pointers that are not 8-byte aligned) and as the parity vehicle.
 //
 // Reference semantics: see ldp_common.cuh and include/aldp_cuda.h.
 #include <cuda_runtime.h>
