@@ -63,12 +63,20 @@ struct FastParams {
     int cell_clamp;                            // cell mode: 1 = per-cell clamp, 0 = cut from the code map
     int edge_lo, edge_hi;                      // band rows recounted with the cell clamp (-1: none)
     int row_lo, row_hi;                        // rows readable as neighbours (-1 / rows with halos)
+    // exact division by per-launch constants, n < 2^31: q = (n * m) >> sh
+    // (m = floor(2^sh / d) + 1, sh = 32 + ceil(log2 d); host: magic_div)
+    uint64_t mg_group, mg_bandG, mg_band1, mg_blocks, mg_cell;
+    int sh_group, sh_bandG, sh_band1, sh_blocks, sh_cell;
     int band_rows, bands, blocks;
     int64_t n_tiles;
     uint32_t one;         // 1 at run time: multiplier that keeps integer adds on the FMA pipe
     uint8_t id_code[128];  // id -> code (0 where no code has that id); 7-bit ids for k == 4
     uint8_t id_bin[128];   // id -> histogram bin (colex rank of the code)
 };
+
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, uint64_t m, int sh) {
+    return uint32_t((uint64_t(n) * m) >> sh);
+}
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
     return __byte_perm(a, b, s);
@@ -287,7 +295,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
         int64_t grp;
         uint32_t t_in;
         if (small_t) {
-            const uint32_t q = uint32_t(tt) / group_tiles;
+            const uint32_t q = fdiv(uint32_t(tt), p.mg_group, p.sh_group);
             grp = q;
             t_in = uint32_t(tt) - q * group_tiles;
         } else {
@@ -297,10 +305,11 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
         const int64_t left_ = p.n_images - grp * G;
         const int gi = left_ < G ? int(left_) : G;  // images in this group
         const uint32_t per_band = uint32_t(gi * p.blocks);
-        band_ = int(t_in / per_band);
+        band_ = int(gi == G ? fdiv(t_in, p.mg_bandG, p.sh_bandG) : fdiv(t_in, p.mg_band1, p.sh_band1));
         const int rem_ = int(t_in - uint32_t(band_) * per_band);
-        img_ = int(grp * G) + rem_ / p.blocks;
-        blk_ = rem_ % p.blocks;
+        const int q_ = int(fdiv(uint32_t(rem_), p.mg_blocks, p.sh_blocks));
+        img_ = int(grp * G) + q_;
+        blk_ = rem_ - q_ * p.blocks;
     };
     const int64_t warp_global = int64_t(blockIdx.x) * kFastWarps + warp;
     const int64_t warp_stride = int64_t(gridDim.x) * kFastWarps;
@@ -417,11 +426,11 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
         };
 
         // ---- histogram slots: region address per pixel (or trash) ----
-        const int cell_c0 = CELLS ? c0 / p.cell_cols : 0;
+        const int cell_c0 = CELLS ? int(fdiv(uint32_t(c0), p.mg_cell, p.sh_cell)) : 0;
         uint32_t slot[LC];
         // one divide per lane: the lane's columns are consecutive, so the
         // cell index / in-cell offset advance by carries (cell_cols >= 3)
-        int cc = CELLS ? y / p.cell_cols : 0, in = CELLS ? y - cc * p.cell_cols : 0;
+        int cc = CELLS ? int(fdiv(uint32_t(y), p.mg_cell, p.sh_cell)) : 0, in = CELLS ? y - cc * p.cell_cols : 0;
 #pragma unroll
         for (int s = 0; s < LC; ++s) {
             const int col = y + s;

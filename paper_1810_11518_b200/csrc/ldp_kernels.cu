@@ -233,6 +233,17 @@ static aldp_status validate(const aldp_ldp_args* a, int* grid_r, int* grid_c, bo
     return ALDP_OK;
 }
 
+// Exact unsigned division by d for dividends below 2^31 as (n * m) >> sh:
+// sh = 32 + ceil(log2 d), m = floor(2^sh / d) + 1. The error term n(m - 2^sh/d)
+// / 2^sh < 2^31 / 2^sh <= 1 / (2d) never crosses an integer (Granlund-Montgomery).
+static void magic_div(uint32_t d, uint64_t& m, int& sh) {
+    if (d == 0) d = 1;
+    int l = 0;
+    while ((uint64_t(1) << l) < d) ++l;
+    sh = 32 + l;
+    m = (uint64_t(1) << sh) / d + 1;  // < 2^33 + 1 (2^l < 2d), so n * m < 2^64
+}
+
 // lbp: the LBP descriptor (256 bins, k ignored); internally k == 0.
 static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st, bool lbp) {
     int grid_r = 1, grid_c = 1;
@@ -293,6 +304,14 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
         }
         p.bands = (a->rows + p.band_rows - 1) / p.band_rows;
         p.n_tiles = int64_t(a->n_images) * p.bands * p.blocks;
+        {
+            const int G = (p.blocks & 1) ? 2 : 1;
+            magic_div(uint32_t(int64_t(G) * p.bands * p.blocks), p.mg_group, p.sh_group);
+            magic_div(uint32_t(G * p.blocks), p.mg_bandG, p.sh_bandG);
+            magic_div(uint32_t(p.blocks), p.mg_band1, p.sh_band1);
+            magic_div(uint32_t(p.blocks), p.mg_blocks, p.sh_blocks);
+            magic_div(uint32_t(a->cell_cols ? a->cell_cols : 1), p.mg_cell, p.sh_cell);
+        }
         p.one = 1;
         for (int id = 0; id < 128; ++id) p.id_code[id] = p.id_bin[id] = 0;
         for (int c = 0; c < 256 && k; ++c)
