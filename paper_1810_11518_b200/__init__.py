@@ -54,7 +54,8 @@ class ResponsePath(enum.IntEnum):
 
 
 class Descriptor(enum.Enum):
-    """aldp::Descriptor (descriptors.hpp:13). Lbp is not on the B200 path."""
+    """aldp::Descriptor (descriptors.hpp:13). All three run on the B200 (Lbp: the
+    LBP instantiation of the fast kernel; Ldp / Aldp: the LDP kernel)."""
     Lbp = "LBP"
     Ldp = "LDP"
     Aldp = "ALDP"

@@ -20,3 +20,12 @@ L="python bench.py --config c5lbp --images 4096 --steps 3 --warmup 3 --no-cpu --
 timeout 300 $L > gpurun_out/${TAG}_sub_lbp.json 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:ldp_fast -s 3 -c 1 -o gpurun_out/${TAG}_full_lbp $L > gpurun_out/${TAG}_ncu_full_lbp.log 2>&1; echo "ncu-full-lbp rc=$?"
 F="python tools/bench_field.py --images 512 --steps 2 --warmup 1"
 timeout 600 $F > /dev/null 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:response_field_row -s 2 -c 1 -o gpurun_out/${TAG}_full_field $F > gpurun_out/${TAG}_ncu_field.log 2>&1; echo "ncu-field rc=$?"
+# summarise on the box and drop the .ncu-rep files (gpurun copies back <= 64 MiB)
+for r in full full_lbp full_field; do
+  [ -f gpurun_out/${TAG}_$r.ncu-rep ] || continue
+  L=""; [ "$r" == "full" ] && L=gpurun_out/${TAG}_launches.csv
+  python tools/ncu_summary.py gpurun_out/${TAG}_$r.ncu-rep gpurun_out/${TAG}_ncu_$r.md $L > /dev/null 2>&1
+  [ "$r" == "full" ] && ncu -i gpurun_out/${TAG}_$r.ncu-rep --page source --csv --print-source sass > gpurun_out/${TAG}_source_sass.csv 2>/dev/null
+  rm -f gpurun_out/${TAG}_$r.ncu-rep
+done
+du -sh gpurun_out
