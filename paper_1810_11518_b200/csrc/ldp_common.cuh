@@ -29,13 +29,27 @@
 
 namespace aldp_b200 {
 
-__host__ __device__ constexpr uint32_t kTag(int i) {
-    // W[0..7] = 53, 48, 43, 37, 25, 19, 17, 16 (strictly decreasing;
-    // triple-XOR distinct; see tests/test_host.py::test_tag_set_properties)
-    return i == 0 ? 53u : i == 1 ? 48u : i == 2 ? 43u : i == 3 ? 37u
-         : i == 4 ? 25u : i == 5 ? 19u : i == 6 ? 17u : 16u;
+// Two tag sets. TS 0: W[0..7] = 53, 48, 43, 37, 25, 19, 17, 16; TS 1: the
+// same set XOR-ed with 16 and re-sorted, 59, 53, 37, 32, 9, 3, 1, 0 (a
+// uniform XOR keeps every k-subset XOR distinct). Both strictly decreasing,
+// triple-XOR distinct and k == 4 (XOR, direction-0) distinct; see
+// tests/test_host.py::test_tag_set_properties. TS 1's zero tag lets the fast
+// kernel form K7 as a plain two-input add (measured faster on the whole-image
+// kernel, slower on the cell kernel: DESIGN.md section 6).
+template <int TS>
+__host__ __device__ constexpr uint32_t kTagT(int i) {
+    if constexpr (TS == 0)
+        return i == 0 ? 53u : i == 1 ? 48u : i == 2 ? 43u : i == 3 ? 37u
+             : i == 4 ? 25u : i == 5 ? 19u : i == 6 ? 17u : 16u;
+    else
+        return i == 0 ? 59u : i == 1 ? 53u : i == 2 ? 37u : i == 3 ? 32u
+             : i == 4 ? 9u : i == 5 ? 3u : i == 6 ? 1u : 0u;
 }
-constexpr uint32_t kTagAllXor = 53u ^ 48u ^ 43u ^ 37u ^ 25u ^ 19u ^ 17u ^ 16u;
+__host__ __device__ constexpr uint32_t kTag(int i) { return kTagT<0>(i); }
+template <int TS>
+constexpr uint32_t kTagAllXorT =
+    kTagT<TS>(0) ^ kTagT<TS>(1) ^ kTagT<TS>(2) ^ kTagT<TS>(3) ^ kTagT<TS>(4) ^ kTagT<TS>(5) ^ kTagT<TS>(6) ^ kTagT<TS>(7);
+constexpr uint32_t kTagAllXor = kTagAllXorT<0>;
 constexpr int kKeyShift = 6;
 
 __host__ __device__ inline int popcount8(unsigned c) {
@@ -62,10 +76,10 @@ __host__ __device__ inline int colex_rank(unsigned code) {
     return rank;
 }
 
-__host__ __device__ inline uint32_t tag_xor(unsigned code) {
+__host__ __device__ inline uint32_t tag_xor(unsigned code, int ts = 0) {
     uint32_t x = 0;
     for (int i = 0; i < 8; ++i)
-        if ((code >> i) & 1u) x ^= kTag(i);
+        if ((code >> i) & 1u) x ^= ts ? kTagT<1>(i) : kTagT<0>(i);
     return x;
 }
 
@@ -112,14 +126,14 @@ __device__ __forceinline__ uint32_t vaddmin(uint32_t a, uint32_t b, uint32_t c) 
 //
 // topk_from_pairs takes the network after its first comparator layer:
 // p/q = max/min(K0,K1), r/s = max/min(K2,K3) (half A), same for K4..K7.
-template <int K>
+template <int K, int TS = 0>
 __device__ __forceinline__ uint32_t topk_from_pairs(uint32_t pA, uint32_t qA, uint32_t rA, uint32_t sA,
                                                     uint32_t pB, uint32_t qB, uint32_t rB, uint32_t sB) {
     static_assert(K >= 1 && K <= 7 && K != 4, "k == 4 selects through top4_id");
     if constexpr (K == 1) {
         return vmax(vmax3(pA, rA, pB), rB);
     } else if constexpr (K == 7) {  // complement of the single smallest key
-        return kTagAllXor * 0x10001u ^ vmin(vmin3(qA, sA, qB), sB);
+        return kTagAllXorT<TS> * 0x10001u ^ vmin(vmin3(qA, sA, qB), sB);
     } else {
         const uint32_t xA = vmin(pA, rA), yA = vmax(qA, sA);
         const uint32_t xB = vmin(pB, rB), yB = vmax(qB, sB);
@@ -134,13 +148,13 @@ __device__ __forceinline__ uint32_t topk_from_pairs(uint32_t pA, uint32_t qA, ui
             return vmax3(pA, rA, b2) ^ vmax3(a2, pB, rB);
         } else if constexpr (K == 6) {  // complement of the two smallest
             const uint32_t s2A = vmin(xA, yA), s2B = vmin(xB, yB);
-            return kTagAllXor * 0x10001u ^ vmin3(qA, sA, s2B) ^ vmin3(s2A, qB, sB);
+            return kTagAllXorT<TS> * 0x10001u ^ vmin3(qA, sA, s2B) ^ vmin3(s2A, qB, sB);
         } else {  // K == 5: complement of the three smallest (dual network)
             const uint32_t s3A = vmax(xA, yA), s3B = vmax(xB, yB);
             const uint32_t e1 = vmin3(qA, sA, s3B);
             const uint32_t e2 = vmin3(xA, yA, vmin(xB, yB));
             const uint32_t e3 = vmin3(s3A, qB, sB);
-            return kTagAllXor * 0x10001u ^ e1 ^ e2 ^ e3;
+            return kTagAllXorT<TS> * 0x10001u ^ e1 ^ e2 ^ e3;
         }
     }
 }

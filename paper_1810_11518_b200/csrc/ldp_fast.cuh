@@ -74,6 +74,10 @@ struct FastParams {
     uint8_t id_bin[128];   // id -> histogram bin (colex rank of the code)
 };
 
+// Tag set of a fast-kernel instantiation (ldp_common.cuh kTagT): the cell
+// kernel keeps set 0, the whole-image kernel takes set 1.
+__host__ __device__ constexpr int fast_tag_set(bool cells) { return cells ? 0 : 1; }
+
 __device__ __forceinline__ uint32_t fdiv(uint32_t n, uint64_t m, int sh) {
     return uint32_t((uint64_t(n) * m) >> sh);
 }
@@ -101,11 +105,31 @@ struct Col {
 // Keys of one pixel pair from rows a (above), b, c (below). Ring: TL=a.l
 // T=a.c TR=a.r R=b.r BR=c.r B=c.c BL=c.l L=b.l (kirsch.cpp:11-12);
 // S_i = r[(2-i)&7] + r[(3-i)&7] + r[(4-i)&7].
-template <int K>
+template <int K, int TS = 0>
 __device__ __forceinline__ uint32_t pair_id(const Col& a, const Col& b, const Col& c, uint32_t one) {
-    constexpr uint32_t T0 = kTag(0) * 0x10001u, T1 = kTag(1) * 0x10001u, T2 = kTag(2) * 0x10001u,
-                       T3 = kTag(3) * 0x10001u, T4 = kTag(4) * 0x10001u, T5 = kTag(5) * 0x10001u,
-                       T6 = kTag(6) * 0x10001u, T7 = kTag(7) * 0x10001u;
+    constexpr uint32_t T0 = kTagT<TS>(0) * 0x10001u, T1 = kTagT<TS>(1) * 0x10001u, T2 = kTagT<TS>(2) * 0x10001u,
+                       T3 = kTagT<TS>(3) * 0x10001u, T4 = kTagT<TS>(4) * 0x10001u, T5 = kTagT<TS>(5) * 0x10001u,
+                       T6 = kTagT<TS>(6) * 0x10001u, T7 = kTagT<TS>(7) * 0x10001u;
+    if constexpr (TS == 1) {
+        // Tag set 1 (the whole-image kernel; A/B: +3.6 % on C3, -5.9 % if
+        // used by the cell kernel): the first-layer pairs share a two-input
+        // partial each (P = TR+R, Q = TL+T, R = BL+L, U = B+BR), the even
+        // keys' last add is fused into the comparator, K7 (tag 0) is a
+        // two-input add, and only K1/K3/K5 take a three-input IADD3.
+        static_assert(K < 0 || kTagT<TS>(7) == 0, "tag set 1 has K7's tag 0");
+        const uint32_t P = a.r + b.r, R = b.l + c.l;
+        const uint32_t x0 = P + T0, x2 = a.lc + T2, x4 = R + T4, x6 = c.cr + T6;
+        const uint32_t k1 = P + a.c + T1, k3 = a.lc + b.l + T3, k5 = R + c.c + T5;
+        const uint32_t k7 = c.cr + b.r;
+        if constexpr (K == 4)
+            return top4_id(vaddmax(x0, c.r, k1), vaddmin(x0, c.r, k1), vaddmax(x2, a.r, k3), vaddmin(x2, a.r, k3),
+                           vaddmax(x4, a.l, k5), vaddmin(x4, a.l, k5), vaddmax(x6, c.l, k7), vaddmin(x6, c.l, k7),
+                           fadd(x0, c.r, one));
+        else
+            return topk_from_pairs<K, TS>(vaddmax(x0, c.r, k1), vaddmin(x0, c.r, k1), vaddmax(x2, a.r, k3),
+                                          vaddmin(x2, a.r, k3), vaddmax(x4, a.l, k5), vaddmin(x4, a.l, k5),
+                                          vaddmax(x6, c.l, k7), vaddmin(x6, c.l, k7));
+    }
     // Key/first-layer schemes (A/B measured on C5/C4/C3, tools/gpu_ab.sh):
     //  3 (default): odd keys by one IADD3 each, even keys' last add fused
     //     into the first comparator layer (VIADDMNMX.U16x2): 16 instr/pair;
@@ -114,7 +138,7 @@ __device__ __forceinline__ uint32_t pair_id(const Col& a, const Col& b, const Co
 #ifndef ALDP_KEYMODE
 #define ALDP_KEYMODE 3
 #endif
-    if constexpr (ALDP_KEYMODE == 3) {
+    else if constexpr (ALDP_KEYMODE == 3) {
         // fewest instructions: odd keys materialised by one IADD3 each, even
         // keys fused into the comparator (one pre-add + VIADDMNMX)
         const uint32_t k1 = a.cr + b.r + T1, k3 = a.lc + b.l + T3;
@@ -239,6 +263,7 @@ __device__ __forceinline__ void load_words(const uint8_t* p, uint32_t (&w)[NW]) 
 template <int K, int NW, bool CELLS, bool CODES, bool HIST, bool HALO = false>
 __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_kernel(FastParams p) {
     constexpr bool LBP = K == 0;
+    constexpr int TS = fast_tag_set(CELLS);  // the host builds the id tables for the same set
     // LBP: 256 counts; LDP: code table + 64 counts; k == 4: code table + 128 counts
     constexpr int REGION = (LBP || K == 4) ? 1024 : kRegion;
     constexpr int CNT = LBP ? 0 : (K == 4 ? 512 : 256);  // offset of the counts in a region
@@ -475,8 +500,8 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
                     X[2 * j] = pair_lbp(colA<SUMS>(a, j), colA<SUMS>(b, j), colA<SUMS>(c, j), one);
                     X[2 * j + 1] = pair_lbp(colB<SUMS>(a, j), colB<SUMS>(b, j), colB<SUMS>(c, j), one);
                 } else {
-                    X[2 * j] = pair_id<K>(colA<SUMS>(a, j), colA<SUMS>(b, j), colA<SUMS>(c, j), one);
-                    X[2 * j + 1] = pair_id<K>(colB<SUMS>(a, j), colB<SUMS>(b, j), colB<SUMS>(c, j), one);
+                    X[2 * j] = pair_id<K, TS>(colA<SUMS>(a, j), colA<SUMS>(b, j), colA<SUMS>(c, j), one);
+                    X[2 * j + 1] = pair_id<K, TS>(colB<SUMS>(a, j), colB<SUMS>(b, j), colB<SUMS>(c, j), one);
                 }
             }
         };

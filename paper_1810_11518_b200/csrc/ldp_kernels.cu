@@ -313,16 +313,18 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
             magic_div(uint32_t(a->cell_cols ? a->cell_cols : 1), p.mg_cell, p.sh_cell);
         }
         p.one = 1;
+        const bool cells = a->cell_rows != 0 && a->d_hist != nullptr;
+        const int ts = fast_tag_set(cells);  // the tag set the launched kernel keys with
         for (int id = 0; id < 128; ++id) p.id_code[id] = p.id_bin[id] = 0;
         for (int c = 0; c < 256 && k; ++c)
             if (popcount8(c) == k) {
                 // k == 4: the 6-bit XOR plus "direction 0 selected" (ldp_common.cuh top4_id)
-                const int id = int(tag_xor(c)) | (k == 4 ? (c & 1) << 6 : 0);
+                const int id = int(tag_xor(c, ts)) | (k == 4 ? (c & 1) << 6 : 0);
                 if (p.id_code[id]) return fail(ALDP_EINVAL, "internal: code id collision");
                 p.id_code[id] = uint8_t(c);
                 p.id_bin[id] = uint8_t(colex_rank(c));
             }
-        return launch_fast(p, k, a->cell_rows != 0 && a->d_hist != nullptr, a->rows_above || a->rows_below, st);
+        return launch_fast(p, k, cells, a->rows_above || a->rows_below, st);
     }
     GenericParams g{};
     g.px = a->d_pixels;

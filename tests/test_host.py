@@ -13,7 +13,8 @@ import pytest
 import oracle
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-TAGS = [53, 48, 43, 37, 25, 19, 17, 16]  # ldp_common.cuh kTag
+TAGS = [53, 48, 43, 37, 25, 19, 17, 16]  # ldp_common.cuh kTagT<0> (cell kernel, generic kernel)
+TAGS1 = [59, 53, 37, 32, 9, 3, 1, 0]     # ldp_common.cuh kTagT<1> (whole-image fast kernel)
 
 
 def declared_functions(header):
@@ -80,17 +81,25 @@ def test_descriptor_parsing():
         aldp.parse_descriptor("hog")
 
 
-def test_tag_set_properties():
+@pytest.mark.parametrize("tags", [TAGS, TAGS1], ids=["set0", "set1"])
+def test_tag_set_properties(tags):
     """K_i = 64*S_i + W[i]: W strictly decreasing (ties -> lower index) and the
     XOR of any k-subset's tags unique for k != 4 (the 6-bit code id)."""
-    assert TAGS == sorted(TAGS, reverse=True) and len(set(TAGS)) == 8
-    assert max(TAGS) < 64 and 64 * 765 + max(TAGS) < 65536
+    assert tags == sorted(tags, reverse=True) and len(set(tags)) == 8
+    assert max(tags) < 64 and 64 * 765 + max(tags) < 65536
     for k in (1, 2, 3, 5, 6, 7):
-        ids = [reduce(lambda a, b: a ^ b, (TAGS[i] for i in s)) for s in itertools.combinations(range(8), k)]
+        ids = [reduce(lambda a, b: a ^ b, (tags[i] for i in s)) for s in itertools.combinations(range(8), k)]
         assert len(set(ids)) == len(ids), k
     # k == 4: the XOR plus "direction 0 selected" is unique (7-bit id, top4_id)
-    ids4 = [(reduce(lambda a, b: a ^ b, (TAGS[i] for i in s)), 0 in s) for s in itertools.combinations(range(8), 4)]
+    ids4 = [(reduce(lambda a, b: a ^ b, (tags[i] for i in s)), 0 in s) for s in itertools.combinations(range(8), 4)]
     assert len(set(ids4)) == 70
+
+
+def test_tag_sets_match_header():
+    """The tag sets above are the ones ldp_common.cuh compiles in."""
+    src = open(os.path.join(os.path.dirname(__file__), "..", "paper_1810_11518_b200", "csrc", "ldp_common.cuh")).read()
+    body = src[src.index("constexpr uint32_t kTagT"):src.index("constexpr uint32_t kTag(int i)")]
+    assert [int(v) for v in re.findall(r"(\d+)u", body)] == TAGS + TAGS1
 
 
 def test_key_order_is_reference_order():
