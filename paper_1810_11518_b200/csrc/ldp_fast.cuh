@@ -111,8 +111,8 @@ __device__ __forceinline__ uint32_t pair_id(const Col& a, const Col& b, const Co
                        T3 = kTagT<TS>(3) * 0x10001u, T4 = kTagT<TS>(4) * 0x10001u, T5 = kTagT<TS>(5) * 0x10001u,
                        T6 = kTagT<TS>(6) * 0x10001u, T7 = kTagT<TS>(7) * 0x10001u;
     if constexpr (TS == 1) {
-        // Tag set 1 (the whole-image kernel; A/B: +3.6 % on C3, -5.9 % if
-        // used by the cell kernel): the first-layer pairs share a two-input
+        // Tag set 1 (the whole-image kernel; A/B: +6 % on C3, -5.9 % if used
+        // by the cell kernel): the first-layer pairs share a two-input
         // partial each (P = TR+R, Q = TL+T, R = BL+L, U = B+BR), the even
         // keys' last add is fused into the comparator, K7 (tag 0) is a
         // two-input add, and only K1/K3/K5 take a three-input IADD3.
@@ -129,18 +129,12 @@ __device__ __forceinline__ uint32_t pair_id(const Col& a, const Col& b, const Co
             return topk_from_pairs<K, TS>(vaddmax(x0, c.r, k1), vaddmin(x0, c.r, k1), vaddmax(x2, a.r, k3),
                                           vaddmin(x2, a.r, k3), vaddmax(x4, a.l, k5), vaddmin(x4, a.l, k5),
                                           vaddmax(x6, c.l, k7), vaddmin(x6, c.l, k7));
-    }
-    // Key/first-layer schemes (A/B measured on C5/C4/C3, tools/gpu_ab.sh):
-    //  3 (default): odd keys by one IADD3 each, even keys' last add fused
-    //     into the first comparator layer (VIADDMNMX.U16x2): 16 instr/pair;
-    //  1/2: odd keys fused with their tag as immediate, sums on the FMA
-    //     pipe (IMAD), even keys materialised: 20 instr/pair, fewer on ALU.
-#ifndef ALDP_KEYMODE
-#define ALDP_KEYMODE 3
-#endif
-    else if constexpr (ALDP_KEYMODE == 3) {
-        // fewest instructions: odd keys materialised by one IADD3 each, even
-        // keys fused into the comparator (one pre-add + VIADDMNMX)
+    } else {
+        // Tag set 0 (the cell kernel): odd keys materialised by one IADD3
+        // each, the even keys' last add fused into the first comparator layer
+        // (one pre-add + VIADDMNMX): 16 instructions per pair. Measured and
+        // rejected for this kernel: sums on the FMA pipe
+        // (IMAD), the tag-set-1 scheme above, FMA-pipe slot addresses.
         const uint32_t k1 = a.cr + b.r + T1, k3 = a.lc + b.l + T3;
         const uint32_t k5 = c.lc + b.l + T5, k7 = c.cr + b.r + T7;
         const uint32_t x0 = a.r + b.r + T0, x4 = a.l + b.l + T4;   // + c.r / + c.l fused
@@ -153,24 +147,6 @@ __device__ __forceinline__ uint32_t pair_id(const Col& a, const Col& b, const Co
             return topk_from_pairs<K>(vaddmax(x0, c.r, k1), vaddmin(x0, c.r, k1), vaddmax(x2, a.r, k3),
                                       vaddmin(x2, a.r, k3), vaddmax(x4, c.l, k5), vaddmin(x4, c.l, k5),
                                       vaddmax(x6, c.r, k7), vaddmin(x6, c.r, k7));
-    } else {
-    const uint32_t k0 = fadd(fadd(a.r, b.r, one), c.r, one) + T0;  // TR + R + BR
-    const uint32_t k4 = fadd(fadd(a.l, b.l, one), c.l, one) + T4;  // BL + L + TL
-    uint32_t k2, k6;
-    if constexpr (ALDP_KEYMODE == 2) {
-        k2 = fadd(a.lc, a.r, one) + T2;  // TL + T + TR
-        k6 = fadd(c.lc, c.r, one) + T6;  // BR + B + BL
-    } else {
-        k2 = a.lc + a.r + T2;
-        k6 = c.lc + c.r + T6;
-    }
-    const uint32_t s1 = fadd(a.cr, b.r, one);  // T + TR + R    (k1 - T1)
-    const uint32_t s3 = fadd(a.lc, b.l, one);  // L + TL + T    (k3 - T3)
-    const uint32_t s5 = fadd(c.lc, b.l, one);  // B + BL + L    (k5 - T5)
-    const uint32_t s7 = fadd(c.cr, b.r, one);  // R + BR + B    (k7 - T7)
-    return topk_from_pairs<K>(vaddmax(s1, T1, k0), vaddmin(s1, T1, k0), vaddmax(s3, T3, k2),
-                              vaddmin(s3, T3, k2), vaddmax(s5, T5, k4), vaddmin(s5, T5, k4),
-                              vaddmax(s7, T7, k6), vaddmin(s7, T7, k6));
     }
 }
 
