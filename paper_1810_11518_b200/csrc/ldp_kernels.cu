@@ -109,6 +109,7 @@ __global__ void ldp_generic_kernel(GenericParams p) {
 // --------------------------------------------------------------------------
 }  // namespace aldp_b200
 #include "ldp_fast.cuh"
+#include "ldp_fast_launch.cuh"
 namespace aldp_b200 {
 
 // --------------------------------------------------------------------------
@@ -127,38 +128,11 @@ static int n_sms() {
     return cache[dev];
 }
 
-template <int K, int NW, bool CELLS, bool CODES, bool HIST, bool HALO>
-static aldp_status launch_fast_t(const FastParams& p, cudaStream_t st) {
-    auto kern = ldp_fast_kernel<K, NW, CELLS, CODES, HIST, HALO>;
-    constexpr int NSEG = 32 / (kTileCols / (4 * NW));
-    constexpr int REGION = (K == 0 || K == 4) ? 1024 : kRegion;  // LBP: 256 counts, k == 4: 7-bit ids
-    const size_t smem = size_t(kFastWarps) * NSEG * kSegRegions * REGION + REGION;  // + alignment slack
-    // The shared-memory opt-in is a per-device function attribute: set it once
-    // per device this process launches on (several GPUs in one process work).
-    constexpr int kMaxDev = 64;
-    static std::once_flag once[kMaxDev];
-    static cudaError_t attr_err[kMaxDev];
-    static int per_sm_dev[kMaxDev];
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev < 0 || dev >= kMaxDev) return cuda_fail(cudaErrorInvalidDevice, "fast kernel setup");
-    std::call_once(once[dev], [&] {
-        int ps = 1;
-        attr_err[dev] = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        if (attr_err[dev] == cudaSuccess)
-            attr_err[dev] = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, kFastWarps * 32, smem);
-        per_sm_dev[dev] = ps < 1 ? 1 : ps;
-    });
-    if (attr_err[dev] != cudaSuccess) return cuda_fail(attr_err[dev], "fast kernel setup");
-    const int per_sm = per_sm_dev[dev];
-    const int64_t warp_tiles = (p.n_tiles + NSEG - 1) / NSEG;
-    const int64_t want = (warp_tiles + kFastWarps - 1) / kFastWarps;
-    const int grid = int(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(per_sm) * n_sms())));
-    kern<<<grid, kFastWarps * 32, smem, st>>>(p);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return cuda_fail(e, "ldp_fast_kernel launch");
-    return ALDP_OK;
-}
+// launch_fast_t<...> (ldp_fast_launch.cuh): the cell-histogram
+// instantiations are compiled in ldp_fast_cells.cu (their own ptxas
+// options), the rest here.
+int fast_n_sms() { return n_sms(); }
+ALDP_FAST_CELL_INSTANTIATIONS(extern template)
 
 template <int K, int NW, bool HALO>
 static aldp_status launch_fast_kw(const FastParams& p, bool cells, cudaStream_t st) {
