@@ -68,6 +68,12 @@ WORKLOAD_NAMES = {
 }
 
 
+def workload_name(cfg, k):
+    """The config's workload text, with the k actually run (--k overrides)."""
+    name = WORKLOAD_NAMES[cfg]
+    return name if k == 0 else name.replace("LDP k=3", f"LDP k={k}")
+
+
 def hist_bytes_per_image(rows, cols, k, cr, cc):
     from math import comb
     cells = 1 if cr == 0 else (rows // cr) * (cols // cc)
@@ -208,7 +214,7 @@ def run_reference(args, cfg_name):
         "unit": "Mpixel/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic (numpy face-like, same recipe)",
-        "config": {"workload": WORKLOAD_NAMES[cfg_name], "images_per_step": int(px.shape[0]),
+        "config": {"workload": workload_name(cfg_name, k), "images_per_step": int(px.shape[0]),
                    "parallelism": f"{threads} host threads over images", "cpu_only": True},
         "cpu_baseline": {"value": round(mpx, 3), "unit": "Mpixel/s", "cores": threads, "kind": kind,
                          "sample": f"{px.shape[0]} images of {px.shape[1]}x{px.shape[2]} per step, "
@@ -445,7 +451,7 @@ def main():
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic (device generator, seeded, keyed by global image index)",
-        "config": {"workload": WORKLOAD_NAMES[args.config], "images": n, "rows": rows, "cols": cols,
+        "config": {"workload": workload_name(args.config, k), "images": n, "rows": rows, "cols": cols,
                    "k": k, "cell": [cr, cc], "parallelism": f"image shards x{world}",
                    "l2": "inputs larger than L2 (no flush)" if n * rows * cols > 4 * 126e6 else
                          "inputs smaller than L2: repeated steps hit L2",
