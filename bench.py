@@ -438,6 +438,18 @@ def main():
     checks = {"hist_weighted_sum": int(sums[0]), "code_sum": int(sums[1]),
               "note": "sum over all images of bin-index-weighted counts, and of code bytes"}
 
+    # kernels per ldp_batch call: cell histograms over a frame whose rows
+    # overhang the cell grid run the grid and the remainder rows (codes only)
+    # as two launches (ldp_kernels.cu run_batch)
+    # (small batches only: under 64 tiles per warp segment, as run_batch decides)
+    seg_slots = torch.cuda.get_device_properties(dev).multi_processor_count * 2 * 8 * 2
+
+    def kernels_of(m):
+        tiles = m * (-(-rows // cr) if cr else 1) * -(-cols // 128)
+        return 2 if cr and rows % cr and tiles < 64 * seg_slots else 1
+
+    kernels_per_step = sum(kernels_of(b - a) for a, b in bounds)
+
     # ---- roofline of the dominant kernel (one launch = this rank's shard) ----
     hbm, peak_src = measured_peaks()
     traffic_bpp, traffic_src = ncu_traffic_bpp()
@@ -466,9 +478,9 @@ def main():
                      "peak_source": peak_src,
                      "bytes_per_pixel": round(2.0 + bpp_hist, 4),
                      "launch_ms": round(launch_ms, 4), "launch_median_ms": round(launch_median_ms, 4),
-                     "launches_per_step": n_chunks},
+                     "launches_per_step": kernels_per_step},
         "clocks": clocks,
-        "gpu_launches": args.steps * n_chunks,
+        "gpu_launches": args.steps * kernels_per_step,
     }
 
     # ---- end to end through the host C-ABI (pinned host buffers) ----

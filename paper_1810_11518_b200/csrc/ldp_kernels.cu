@@ -218,6 +218,46 @@ static void magic_div(uint32_t d, uint64_t& m, int& sh) {
     m = (uint64_t(1) << sh) / d + 1;  // < 2^33 + 1 (2^l < 2d), so n * m < 2^64
 }
 
+// Band geometry, tile order, exact-division constants and id tables of a
+// fast-kernel launch over n_images frames of p.rows rows, then the launch.
+// cells: cell histograms (the cell kernel and tag set 0); halo: p is a band
+// view whose edge rows may see real rows (row_lo / row_hi).
+static aldp_status finish_fast(FastParams& p, int n_images, int cell_rows, int cell_cols, int k, bool cells,
+                               bool halo, cudaStream_t st) {
+    p.band_rows = cell_rows ? cell_rows : 128;
+    if (!cell_rows) {
+        // Small batches (a few frames per call): shorter bands until the
+        // tiles fill every warp slot once (2 tiles per warp, 2 CTAs of 8
+        // warps per SM); each band costs two recounted edge rows.
+        const int64_t slots = int64_t(n_sms()) * 2 * kFastWarps * 2;
+        while (p.band_rows > 16 &&
+               int64_t(n_images) * ((p.rows + p.band_rows - 1) / p.band_rows) * p.blocks < slots)
+            p.band_rows /= 2;
+    }
+    p.bands = (p.rows + p.band_rows - 1) / p.band_rows;
+    p.n_tiles = int64_t(n_images) * p.bands * p.blocks;
+    {
+        const int G = (p.blocks & 1) ? 2 : 1;
+        magic_div(uint32_t(int64_t(G) * p.bands * p.blocks), p.mg_group, p.sh_group);
+        magic_div(uint32_t(G * p.blocks), p.mg_bandG, p.sh_bandG);
+        magic_div(uint32_t(p.blocks), p.mg_band1, p.sh_band1);
+        magic_div(uint32_t(p.blocks), p.mg_blocks, p.sh_blocks);
+        magic_div(uint32_t(cell_cols ? cell_cols : 1), p.mg_cell, p.sh_cell);
+    }
+    p.one = 1;
+    const int ts = fast_tag_set(cells);  // the tag set the launched kernel keys with
+    for (int id = 0; id < 128; ++id) p.id_code[id] = p.id_bin[id] = 0;
+    for (int c = 0; c < 256 && k; ++c)
+        if (popcount8(c) == k) {
+            // k == 4: the 6-bit XOR plus "direction 0 selected" (ldp_common.cuh top4_id)
+            const int id = int(tag_xor(c, ts)) | (k == 4 ? (c & 1) << 6 : 0);
+            if (p.id_code[id]) return fail(ALDP_EINVAL, "internal: code id collision");
+            p.id_code[id] = uint8_t(c);
+            p.id_bin[id] = uint8_t(colex_rank(c));
+        }
+    return launch_fast(p, k, cells, halo, st);
+}
+
 // lbp: the LBP descriptor (256 bins, k ignored); internally k == 0.
 static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st, bool lbp) {
     int grid_r = 1, grid_c = 1;
@@ -266,39 +306,47 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
         p.grid_r = grid_r;
         p.grid_c = grid_c;
         p.blocks = (a->cols + kTileCols - 1) / kTileCols;
-        p.band_rows = a->cell_rows ? a->cell_rows : 128;
-        if (!a->cell_rows) {
-            // Small batches (a few frames per call): shorter bands until the
-            // tiles fill every warp slot once (2 tiles per warp, 2 CTAs of 8
-            // warps per SM); each band costs two recounted edge rows.
-            const int64_t slots = int64_t(n_sms()) * 2 * kFastWarps * 2;
-            while (p.band_rows > 16 &&
-                   int64_t(a->n_images) * ((a->rows + p.band_rows - 1) / p.band_rows) * p.blocks < slots)
-                p.band_rows /= 2;
+        // Cell histograms with rows below the cell grid (490 = 6 x 81 + 4 for
+        // the 7x6 grid of a 640x490 frame): the grid rows run as one launch and
+        // the short remainder as a second, codes-only launch. Warps take tiles
+        // round-robin; with the short band mixed in, a warp that drew only
+        // full-height tiles set the end of the kernel on small batches (C2:
+        // its 8 tiles against a mean of 6.5). Only the grid launch's last row
+        // sees a clamped row below it; it is a cell edge row (its histogram
+        // uses the cell clamp anyway) and its code is rewritten by the second
+        // launch, which starts two rows above the grid's end with a real row
+        // above it. cell_from_map counts map codes, so it keeps one launch.
+        // Only for small batches (under kSplitTiles tiles per warp segment):
+        // the remainder launch recomputes ~1 % of the pixels, more than the
+        // imbalance costs a large batch (C5: -0.5 % split, C2: +4.7 %).
+        constexpr int64_t kSplitTiles = 64;
+        const int grid_rows = grid_r * a->cell_rows;
+        const int64_t tiles = int64_t(a->n_images) * ((a->rows + a->cell_rows - 1) / std::max(a->cell_rows, 1)) *
+                              ((a->cols + kTileCols - 1) / kTileCols);
+        const int64_t seg_slots = int64_t(n_sms()) * 2 * kFastWarps * 2;
+        if (a->cell_rows && !a->cell_from_map && grid_rows < a->rows && tiles < kSplitTiles * seg_slots) {
+            FastParams q = p;
+            p.rows = grid_rows;
+            p.row_hi = grid_rows - 1;
+            if (aldp_status s1 = finish_fast(p, a->n_images, a->cell_rows, a->cell_cols, k, a->d_hist != nullptr,
+                                             a->rows_above != 0, st);
+                s1 != ALDP_OK)
+                return s1;
+            if (!a->d_codes) return ALDP_OK;
+            const int start = grid_rows - 2;  // >= 1: cells are >= 3 rows
+            q.px = a->d_pixels + int64_t(start) * a->pitch;
+            q.rows = a->rows - start;
+            q.codes = a->d_codes + int64_t(start) * a->codes_pitch;
+            q.hist = nullptr;
+            q.cell_rows = q.cell_cols = 0;
+            q.grid_r = q.grid_c = 1;
+            q.edge_lo = q.edge_hi = -1;
+            q.row_lo = -1;
+            q.row_hi = q.rows - 1 + (a->rows_below ? 1 : 0);
+            return finish_fast(q, a->n_images, 0, 0, k, false, true, st);
         }
-        p.bands = (a->rows + p.band_rows - 1) / p.band_rows;
-        p.n_tiles = int64_t(a->n_images) * p.bands * p.blocks;
-        {
-            const int G = (p.blocks & 1) ? 2 : 1;
-            magic_div(uint32_t(int64_t(G) * p.bands * p.blocks), p.mg_group, p.sh_group);
-            magic_div(uint32_t(G * p.blocks), p.mg_bandG, p.sh_bandG);
-            magic_div(uint32_t(p.blocks), p.mg_band1, p.sh_band1);
-            magic_div(uint32_t(p.blocks), p.mg_blocks, p.sh_blocks);
-            magic_div(uint32_t(a->cell_cols ? a->cell_cols : 1), p.mg_cell, p.sh_cell);
-        }
-        p.one = 1;
-        const bool cells = a->cell_rows != 0 && a->d_hist != nullptr;
-        const int ts = fast_tag_set(cells);  // the tag set the launched kernel keys with
-        for (int id = 0; id < 128; ++id) p.id_code[id] = p.id_bin[id] = 0;
-        for (int c = 0; c < 256 && k; ++c)
-            if (popcount8(c) == k) {
-                // k == 4: the 6-bit XOR plus "direction 0 selected" (ldp_common.cuh top4_id)
-                const int id = int(tag_xor(c, ts)) | (k == 4 ? (c & 1) << 6 : 0);
-                if (p.id_code[id]) return fail(ALDP_EINVAL, "internal: code id collision");
-                p.id_code[id] = uint8_t(c);
-                p.id_bin[id] = uint8_t(colex_rank(c));
-            }
-        return launch_fast(p, k, cells, a->rows_above || a->rows_below, st);
+        return finish_fast(p, a->n_images, a->cell_rows, a->cell_cols, k, a->cell_rows != 0 && a->d_hist != nullptr,
+                           a->rows_above || a->rows_below, st);
     }
     GenericParams g{};
     g.px = a->d_pixels;
