@@ -324,7 +324,7 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
         const int64_t tiles = int64_t(a->n_images) * ((a->rows + a->cell_rows - 1) / std::max(a->cell_rows, 1)) *
                               ((a->cols + kTileCols - 1) / kTileCols);
         const int64_t seg_slots = int64_t(n_sms()) * 2 * kFastWarps * 2;
-        if (a->cell_rows && !a->cell_from_map && grid_rows < a->rows && tiles < kSplitTiles * seg_slots) {
+        if (a->cell_rows && grid_r >= 1 && !a->cell_from_map && grid_rows < a->rows && tiles < kSplitTiles * seg_slots) {
             FastParams q = p;
             p.rows = grid_rows;
             p.row_hi = grid_rows - 1;
