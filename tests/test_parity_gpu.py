@@ -513,3 +513,36 @@ print(json.dumps(out))
     assert r.returncode == 0, r.stderr[-3000:]
     res = json.loads(r.stdout.strip().splitlines()[-1])
     assert all(res), res
+
+
+@pytest.mark.parametrize("k", [0, 3, 4])
+@pytest.mark.parametrize("rows,cell", [(490, (81, 91)), (100, (3, 64)), (37, (9, 40)), (130, (64, 64))])
+def test_small_batch_split_launch(k, rows, cell):
+    """Small cell batches whose rows overhang the cell grid run as two
+    launches (grid rows with histograms, remainder rows codes-only from two
+    rows above the grid's end; ldp_kernels.cu run_batch). Every code and
+    every cell count equals the oracle's, including the rows around the
+    grid's end; the same holds for a band view with a real row above and
+    below it (halo = (1, 1))."""
+    cols, n = 300, 5
+    assert rows % cell[0] != 0
+    f = aldp.gen_faces(n, rows + 2, cols, blobs=6, seed=rows + k, device=DEV)
+    torch.cuda.synchronize()
+    tall = f[:, :, :cols].cpu().numpy()
+    # plain frames: the first `rows` rows of each tall frame (k = 0: LBP)
+    px = tall[:, :rows]
+    codes, hist = aldp.ldp_batch(to_dev(px), rows, cols, k=k, cell=cell, codes=True, hist=True)
+    torch.cuda.synchronize()
+    want_c, want_h = oracle.batch(px, k=k, cell=cell)
+    assert np.array_equal(codes[:, :, :cols].cpu().numpy(), want_c), (k, rows, cell)
+    assert np.array_equal(hist.cpu().numpy().astype(np.uint64), want_h), (k, rows, cell)
+    # band view: rows 1 .. rows of one tall frame, real rows above and below
+    dt = to_dev(tall[0])
+    view = dt[:, 1:rows + 1, :]
+    codes, hist = aldp.ldp_batch(view, rows, cols, k=k, cell=cell, codes=True, hist=True, halo=(1, 1))
+    torch.cuda.synchronize()
+    full_c, _ = oracle.batch(tall[:1], k=k, hist=False)
+    assert np.array_equal(codes[0, :, :cols].cpu().numpy(), full_c[0, 1:rows + 1]), (k, rows, cell)
+    # the band's cells are clamped as their own images (windowed_features)
+    _, want_band_h = oracle.batch(tall[:1, 1:rows + 1], k=k, cell=cell, codes=False)
+    assert np.array_equal(hist.cpu().numpy().astype(np.uint64), want_band_h), (k, rows, cell)
