@@ -344,10 +344,18 @@ def ldp_batch(pixels, rows: int, cols: int, k: int = 3, cell: Tuple[int, int] = 
     if codes is not None:
         if codes.dtype != torch.uint8 or codes.dim() != 3 or not codes.is_contiguous():
             raise ValueError("codes must be a contiguous uint8 tensor [n, rows, pitch]")
+        if codes.device != pixels.device:
+            raise ValueError(f"codes is on {codes.device}, pixels on {pixels.device}")
+        if codes.shape[0] < n or codes.shape[1] < rows or codes.shape[2] < cols:
+            raise ValueError(f"codes tensor {tuple(codes.shape)} does not cover ({n}, {rows}, {cols})")
         a.d_codes = codes.data_ptr()
         a.codes_pitch = codes.shape[2]
         a.codes_img_stride = codes.shape[1] * codes.shape[2]
     if hist is not None:
+        if hist.dtype not in (torch.int32, torch.uint32):
+            raise ValueError(f"hist must be int32 or uint32, got {hist.dtype}")
+        if hist.device != pixels.device:
+            raise ValueError(f"hist is on {hist.device}, pixels on {pixels.device}")
         if hist.numel() < n * cells * nb or not hist.is_contiguous():
             raise ValueError("hist tensor too small or not contiguous")
         a.d_hist = hist.data_ptr()

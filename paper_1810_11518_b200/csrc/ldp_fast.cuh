@@ -42,12 +42,31 @@ constexpr int kFastWarps = 8;
 constexpr int kTileCols = 128;
 constexpr int kMaxTileCells = 5;
 constexpr uint32_t kScaleMask = 0x3FC03FC0u;  // bytes 0 and 2 of a word, scaled by 64
-// Per-segment shared layout: kMaxTileCells regions + 1 trash region; a region
-// is [id->code table copy (256 B) | counts (256 B)].
-constexpr int kRegion = 512;
+// Per-segment shared layout: kMaxTileCells regions + 1 trash region
+// (FastLayout below).
 constexpr int kSegRegions = kMaxTileCells + 1;
-constexpr int kSegSmem = kSegRegions * kRegion;  // 2 KB
 constexpr int kFixList = 16;                      // border columns per segment (max)
+// Shared-memory layout of one fast-kernel CTA (the launcher sizes the
+// dynamic allocation from it): per (warp, segment) kSegRegions regions, one
+// per cell a tile can touch plus a trash region. LDP region: a copy of the
+// id -> code table, then the counts (CNT bytes in), so one slot address
+// serves the code lookup (LDS [a - CNT]) and the count (RED [a]). LBP: 256
+// counts. Each region's table and counts are stored XOR-permuted by a bank
+// skew (slot_skew) so that lanes of different segments or cells that hold
+// the same id hit different banks.
+template <int K, int NW>
+struct FastLayout {
+    static constexpr int NT = K == 0 ? 256 : (K == 4 ? 128 : 64);  // table entries (codes / ids)
+    static constexpr int CNT = K == 0 ? 0 : NT * 4;                 // offset of the counts in a region
+    static constexpr int REGION = K == 0 ? 1024 : 2 * NT * 4;
+    static constexpr int NSEG = 32 / (kTileCols / (4 * NW));
+    static constexpr int SEG_SMEM = kSegRegions * REGION;
+    static constexpr int BYTES = kFastWarps * NSEG * SEG_SMEM + REGION;  // + alignment slack
+};
+
+// Bank skew (word XOR, < 32) of segment `seg`'s region `lc`.
+__host__ __device__ constexpr uint32_t slot_skew(int seg, int lc) { return uint32_t(seg * 16 + lc * 8) & 31u; }
+
 constexpr int kL2Ahead = 12;                      // rows of L2 prefetch ahead of the load
 
 struct FastParams {
@@ -221,6 +240,7 @@ __device__ __forceinline__ void red_shared(uint32_t addr) {
     asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr));
 }
 
+
 template <int NW>
 __device__ __forceinline__ void load_words(const uint8_t* p, uint32_t (&w)[NW]) {
     if constexpr (NW == 1) {
@@ -240,11 +260,8 @@ template <int K, int NW, bool CELLS, bool CODES, bool HIST, bool HALO = false>
 __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_kernel(FastParams p) {
     constexpr bool LBP = K == 0;
     constexpr int TS = fast_tag_set(CELLS);  // the host builds the id tables for the same set
-    // LBP: 256 counts; LDP: code table + 64 counts; k == 4: code table + 128 counts
-    constexpr int REGION = (LBP || K == 4) ? 1024 : kRegion;
-    constexpr int CNT = LBP ? 0 : (K == 4 ? 512 : 256);  // offset of the counts in a region
-    constexpr int NT = LBP ? 256 : (K == 4 ? 128 : 64);  // table entries (codes / ids)
-    constexpr int SEG_SMEM = kSegRegions * REGION;
+    using Lay = FastLayout<K, NW>;
+    constexpr int REGION = Lay::REGION, CNT = Lay::CNT, NT = Lay::NT, SEG_SMEM = Lay::SEG_SMEM;
     constexpr int LC = 4 * NW;              // columns per lane
     constexpr int SEG = kTileCols / LC;     // lanes per segment (tile)
     constexpr int NSEG = 32 / SEG;          // tiles per warp
@@ -254,7 +271,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
 #define ALDP_CELL_SUMS 0
 #endif
     constexpr int SUMS = CELLS ? ALDP_CELL_SUMS : 2;  // measured: all stored sums win only without cells
-    extern __shared__ __align__(512) uint8_t smem[];
+    extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint8_t id_bin[128];
     __shared__ int fix_cols[kFastWarps][NSEG][kFixList];
     __shared__ int fix_n[kFastWarps][NSEG];
@@ -262,20 +279,22 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int seg = lane / SEG, sl = lane % SEG;
     // Regions must be REGION-aligned in the shared window: a slot address is
-    // formed as (code * 4) | region, so the region's low bits must be zero.
-    // The host allocates REGION extra bytes for this alignment.
+    // formed as (id * 4) ^ (region | skew * 4), so the region's low bits must
+    // be zero. The host allocates REGION extra bytes for this alignment.
     const uint32_t raw_base = uint32_t(__cvta_generic_to_shared(smem));
     const uint32_t smem_base = (raw_base + REGION - 1) & ~uint32_t(REGION - 1);
     uint8_t* const smem_al = smem + (smem_base - raw_base);
     const uint32_t seg_base = smem_base + (warp * NSEG + seg) * SEG_SMEM;
 
-    // LDP: id -> code table copies (one per region); zeroed counts.
+    // LDP: id -> code table copies (one per region, in the region's skewed
+    // order); zeroed counts.
     {
         uint32_t* w = reinterpret_cast<uint32_t*>(smem_al);
         const int words = kFastWarps * NSEG * SEG_SMEM / 4;
         for (int i = threadIdx.x; i < words; i += blockDim.x) {
             const int in_region = i & (REGION / 4 - 1);
-            w[i] = (!LBP && in_region < NT) ? uint32_t(p.id_code[in_region]) : 0u;
+            const int region = (i / (REGION / 4)) % kSegRegions, sg = (i / (SEG_SMEM / 4)) % NSEG;
+            w[i] = (!LBP && in_region < NT) ? uint32_t(p.id_code[in_region ^ slot_skew(sg, region)]) : 0u;
         }
         if (!LBP && threadIdx.x < NT) id_bin[threadIdx.x] = p.id_bin[threadIdx.x];
     }
@@ -317,8 +336,16 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
     const uint32_t seg_lane0 = uint32_t(seg * SEG);
     const uint32_t src_prev = seg_lane0 + uint32_t((sl + SEG - 1) % SEG);
     const uint32_t src_next = seg_lane0 + uint32_t((sl + 1) % SEG);
-    const uint32_t trash = seg_base + kMaxTileCells * REGION + CNT;
+    // masked pixels count here; codes-only launches look codes up here too
+    const uint32_t trash = seg_base + kMaxTileCells * REGION + CNT + slot_skew(seg, kMaxTileCells) * 4;
     const uint32_t one = p.one;
+    // Band b of an image -> first row, height, cell row (cell mode: bands
+    // are cell rows, then the rows below the grid, crow == grid_r).
+    auto band_geom = [&](int b, int& r0_, int& h_, int& crow_) {
+        r0_ = b * p.band_rows;
+        h_ = min(p.band_rows, p.rows - r0_);
+        crow_ = CELLS ? b : 0;
+    };
 
     for (int64_t wt = warp_global; NSEG * wt < p.n_tiles; wt += warp_stride) {
         const int64_t tile = NSEG * wt + seg;
@@ -326,8 +353,9 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
         const int64_t t = seg_live ? tile : p.n_tiles - 1;
         int img, band, blk;
         tile_coords(t, img, band, blk);
-        const int r0 = band * p.band_rows;
-        const int seg_rows = seg_live ? min(p.rows, r0 + p.band_rows) - r0 : 0;
+        int r0, band_h, crow;
+        band_geom(band, r0, band_h, crow);
+        const int seg_rows = seg_live ? band_h : 0;
         // warp-wide row count from warp-uniform quantities only (no shuffle),
         // so the row loop's trip count is known uniform
         int n_rows = 0;
@@ -335,18 +363,26 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
         for (int sg = 0; sg < NSEG; ++sg) {
             const int64_t tt = NSEG * wt + sg;
             if (tt < p.n_tiles) {
-                int im_, bnd, bk_;
+                int im_, bnd, bk_, r0_, h_, cr_;
                 tile_coords(tt, im_, bnd, bk_);
-                n_rows = max(n_rows, min(p.rows, bnd * p.band_rows + p.band_rows) - bnd * p.band_rows);
+                band_geom(bnd, r0_, h_, cr_);
+                n_rows = max(n_rows, h_);
             }
         }
         const int c0 = blk * kTileCols;
         const int y = c0 + sl * LC;
         const uint8_t* img_px = p.px + int64_t(img) * p.img_stride;
-        const bool grid_band = !CELLS || band < p.grid_r;
+        const bool grid_band = !CELLS || crow < p.grid_r;
+        const int cell_r0 = crow * p.cell_rows;  // cell mode: the cell row's first image row
         const bool do_hist = HIST && seg_live && grid_band;
 
         // ---- column clamp (image.cpp:36-40) as aligned offsets + selectors ----
+        // Halo word of the segment's edge lanes (last lane: the 4 columns left
+        // of the tile, lane 0: the 4 right of it), loaded from an aligned
+        // window clamped into the row. One byte permute per row turns it into
+        // the u16x2 form the neighbour lane needs -- B form (columns c0-3,
+        // c0-1) on the left, A form (c0+128, c0+130) on the right -- with the
+        // clamp folded into the selector (byte 4 = a zero byte).
         const int last = p.cols - 1;
         int halo_off;
         uint32_t halo_sel;
@@ -354,16 +390,16 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
             const int col = sl == SEG - 1 ? c0 - 4 : c0 + kTileCols;
             const int a = min(max(col, 0), last & ~3);
             halo_off = a;
-            halo_sel = 0;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) halo_sel |= uint32_t(min(max(col + j, 0), last) - a) << (4 * j);
+            const int j0 = sl == SEG - 1 ? 1 : 0;  // B form: columns col+1, col+3; A form: col, col+2
+            const uint32_t s0 = uint32_t(min(max(col + j0, 0), last) - a);
+            const uint32_t s1 = uint32_t(min(max(col + j0 + 2, 0), last) - a);
+            halo_sel = s0 | 0x40u | (s1 << 8) | 0x4000u;
         }
         const bool halo_lane = sl == 0 || sl == SEG - 1;
-        const uint32_t halo_rot = sl == SEG - 1 ? 30u : 6u;  // B form (bytes 1,3) / A form (bytes 0,2)
         // Own columns come from one aligned window of 4*NW bytes; a tile
         // crossing the right image edge selects bytes so columns past it
-        // repeat the last pixel (warp-uniform branch; never taken when the
-        // width is a multiple of 128).
+        // repeat the last pixel (warp-uniform; such a tile is never SIMPLE,
+        // and never occurs when the width is a multiple of 128).
         const bool any_edge = __any_sync(FULL, c0 + kTileCols > p.cols);
         const int own_off = min(y, last & ~(LC - 1));
         uint32_t sel[NW];
@@ -378,36 +414,44 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
             }
         }
 
-        // per-lane row-0 pointers; a row load adds one IMAD.WIDE per pointer
+        // Row loads: a per-lane row pointer that the row loop advances by one
+        // pitch per step (one IADD3 + IMAD.X); the halo word sits at a fixed
+        // distance from it. Rows outside [row_lo, row_hi] are clamped only
+        // where they can occur: the band's first row and the rows past the
+        // image's last one (row loop tail).
+        const int row_lo = HALO ? p.row_lo : 0, row_hi = HALO ? p.row_hi : p.rows - 1;
+        const int64_t pitch = p.pitch;
         const uint8_t* const own_p = img_px + own_off;
-        const uint8_t* const halo_p = img_px + halo_off;
+        const int64_t halo_d = int64_t(halo_off) - own_off;
         const uint8_t* const pf_p = img_px + c0;
-        auto load_raw = [&](int r) -> RawN<NW> {
-            const int rr = HALO ? min(max(r, p.row_lo), p.row_hi) : min(max(r, 0), p.rows - 1);
+        auto row_ptr = [&](int r) { return own_p + int64_t(min(max(r, row_lo), row_hi)) * pitch; };
+        // r: the row's index (for the L2 prefetch of the whole-image kernel)
+        auto load_ptr = [&](const uint8_t* ptr, int r, RawN<NW>& q) {
             if (!CELLS && sl == 1) {  // pull a row further ahead into L2 (measured: pays only without cells)
                 const int ra_ = min(r + kL2Ahead, p.rows - 1);
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(pf_p + (long long)ra_ * p.pitch));
             }
-            RawN<NW> q;
-            load_words<NW>(own_p + (long long)rr * p.pitch, q.w);
-            q.h = halo_lane ? __ldg(reinterpret_cast<const uint32_t*>(halo_p + (long long)rr * p.pitch)) : 0u;
-            return q;
+            load_words<NW>(ptr, q.w);
+            const uint32_t* hp = reinterpret_cast<const uint32_t*>(ptr + halo_d);  // every lane: no predicated moves
+            if (halo_lane) q.h = __ldg(hp);
         };
-        auto unpack = [&](const RawN<NW>& q) -> RowN<NW> {
+        // raw row -> A/B/L/R u16x2 forms, scaled by 64 (byte permutes with a
+        // zero byte, then IMAD shifts on the FMA pipe)
+        auto unpack = [&](auto simple_tag, const RawN<NW>& q) -> RowN<NW> {
+            constexpr bool SIMPLE = decltype(simple_tag)::value;
             uint32_t w[NW];
 #pragma unroll
             for (int j = 0; j < NW; ++j) w[j] = q.w[j];
-            if (any_edge) {
+            if (!SIMPLE && any_edge) {
 #pragma unroll
                 for (int j = 0; j < NW; ++j) w[j] = prmt(q.w[0], q.w[NW - 1], NW == 1 ? sel[j] & 0x3333u : sel[j]);
             }
-            const uint32_t hv = prmt(q.h, q.h, halo_sel);
-            const uint32_t h = __funnelshift_l(hv, hv, halo_rot) & kScaleMask;
+            const uint32_t h = prmt(q.h, 0u, halo_sel) * 64u;
             RowN<NW> r;
 #pragma unroll
             for (int j = 0; j < NW; ++j) {
-                r.A[j] = (w[j] << 6) & kScaleMask;
-                r.B[j] = (w[j] >> 2) & kScaleMask;
+                r.A[j] = prmt(w[j], 0u, 0x4240u) * 64u;  // columns y+4j, y+4j+2
+                r.B[j] = prmt(w[j], 0u, 0x4341u) * 64u;  // columns y+4j+1, y+4j+3
             }
             const uint32_t xb = sl == SEG - 1 ? h : r.B[NW - 1];
             const uint32_t ya = sl == 0 ? h : r.A[0];
@@ -426,7 +470,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
             return r;
         };
 
-        // ---- histogram slots: region address per pixel (or trash) ----
+        // ---- histogram slots: region address | skew per pixel (or trash) ----
         const int cell_c0 = CELLS ? int(fdiv(uint32_t(c0), p.mg_cell, p.sh_cell)) : 0;
         uint32_t slot[LC];
         // one divide per lane: the lane's columns are consecutive, so the
@@ -443,10 +487,12 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
                      (!p.cell_clamp || (!(in == 0 && col > 0) && !(in == p.cell_cols - 1 && col < last)));
                 lc = cc - cell_c0;
             }
-            slot[s] = on ? seg_base + uint32_t(lc) * REGION + CNT : trash;
+            slot[s] = on ? seg_base + uint32_t(lc) * REGION + CNT + slot_skew(seg, lc) * 4 : trash;
         }
         // per-lane code-map pointer at row r0; a row's store adds one IMAD.WIDE
-        uint8_t* const lane_dst =
+        // (advanced one row per step, so the row loop carries no row index)
+        const int64_t cpitch = p.codes_pitch;
+        uint8_t* st =
             CODES ? p.codes + int64_t(img) * p.codes_img_stride + int64_t(r0) * p.codes_pitch + y : nullptr;
         const bool lane_out = seg_live && y < p.cols;
         // widths that are not a multiple of the lane's 4*NW columns: the lane
@@ -465,9 +511,14 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
             for (int q = 0; q < NPAIR; ++q) {
                 const int s_lo = (q >> 1) * 4 + (q & 1), s_hi = s_lo + 2;
                 constexpr uint32_t M = (NT - 1) * 4;
-                ad[s_lo] = ((X[q] * 4u) & M) | slot[s_lo];
-                ad[s_hi] = (LBP ? (X[q] >> 6) & M : __umulhi(X[q], 1u << 18) & M) | slot[s_hi];
+                ad[s_lo] = ((X[q] * 4u) & M) ^ slot[s_lo];
+                ad[s_hi] = (LBP ? (X[q] >> 6) & M : __umulhi(X[q], 1u << 18) & M) ^ slot[s_hi];
             }
+        };
+        // count the lane's pixels at slot addresses ad
+        auto count = [&](const uint32_t (&ad)[LC]) {
+#pragma unroll
+            for (int s = 0; s < LC; ++s) red_shared(ad[s]);
         };
         auto row_ids = [&](const RowN<NW>& a, const RowN<NW>& b, const RowN<NW>& c, uint32_t (&X)[NPAIR]) {
 #pragma unroll
@@ -482,10 +533,21 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
             }
         };
 
-        // SIMPLE (a std::integral_constant) drops the per-lane live/in-image
-        // predicates for warps that need none.
-        auto step = [&](auto simple_tag, const RowN<NW>& a, const RowN<NW>& b, const RowN<NW>& c, int i) {
+        // Cell border rows (windowing.cpp:42 crops every cell): with the
+        // per-cell clamp the band's first / last row counts its histogram with
+        // the outside row replaced by the row itself; the map keeps the
+        // whole-image code. Those two rows are peeled out of the row loop.
+        const bool clamp_top = HIST && CELLS && grid_band && p.edge_lo == 0 && r0 == cell_r0;
+        const bool clamp_bot = HIST && CELLS && grid_band && p.edge_hi >= 0 && r0 + n_rows == cell_r0 + p.cell_rows;
+
+        // One output row. SIMPLE (a std::integral_constant) drops the per-lane
+        // live/in-image predicates for warps that need none; EDGE: 0 = a row
+        // inside the band, 1 / 2 = the band's first / last row, counted with
+        // the cell clamp when `clamp` is set.
+        auto step = [&](auto simple_tag, auto edge_tag, const RowN<NW>& a, const RowN<NW>& b, const RowN<NW>& c,
+                        int i, bool clamp) {
             constexpr bool SIMPLE = decltype(simple_tag)::value;
+            constexpr int EDGE = decltype(edge_tag)::value;
             uint32_t X[NPAIR], ad[LC];
             row_ids(a, b, c, X);
             addrs(X, ad);
@@ -505,52 +567,77 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
                         wd[j] = e[4 * j] + e[4 * j + 1] * 0x100u + e[4 * j + 2] * 0x10000u + e[4 * j + 3] * 0x1000000u;
                 }
                 if (SIMPLE || (live && lane_full)) {
-                    uint8_t* o = lane_dst + (long long)i * p.codes_pitch;
-                    if constexpr (NW == 1) *reinterpret_cast<uint32_t*>(o) = wd[0];
-                    else *reinterpret_cast<uint2*>(o) = make_uint2(wd[0], wd[1]);
+                    if constexpr (NW == 1) *reinterpret_cast<uint32_t*>(st) = wd[0];
+                    else *reinterpret_cast<uint2*>(st) = make_uint2(wd[0], wd[1]);
                 } else if (live && lane_out) {
-                    uint8_t* o = lane_dst + (long long)i * p.codes_pitch;
-                    for (int b = 0; b < p.cols - y; ++b) o[b] = uint8_t(wd[b >> 2] >> (8 * (b & 3)));
+                    for (int b = 0; b < p.cols - y; ++b) st[b] = uint8_t(wd[b >> 2] >> (8 * (b & 3)));
                 }
+                st += cpitch;
             }
             if (HIST) {
-                if (CELLS && (i == p.edge_lo || i == p.edge_hi)) {
-                    // cell border row: count with the outside row clamped to the cell
+                if (EDGE != 0 && clamp) {
                     uint32_t Y[NPAIR], bd[LC];
-                    row_ids(i == p.edge_lo ? b : a, b, i == p.edge_hi ? b : c, Y);
+                    row_ids(EDGE == 1 ? b : a, b, EDGE == 2 ? b : c, Y);
                     addrs(Y, bd);
-                    if (live)
-#pragma unroll
-                        for (int s = 0; s < LC; ++s) red_shared(bd[s]);
+                    if (live) count(bd);
                 } else if (live) {
-#pragma unroll
-                    for (int s = 0; s < LC; ++s) red_shared(ad[s]);
+                    count(ad);
                 }
             }
         };
 
-        // ---- main loop: rows r0 .. r0+n_rows-1, unrolled by 3 ----
+        // ---- rows r0 .. r0+n_rows-1: first row, 3-way unrolled middle, last row ----
+        // Three unpacked rows in registers, three raw rows in flight.
         auto run_rows = [&](auto simple_tag) {
-            RowN<NW> ra = unpack(load_raw(r0 - 1));
-            RowN<NW> rb = unpack(load_raw(r0));
-            RowN<NW> rc = unpack(load_raw(r0 + 1));
-            RawN<NW> q0 = load_raw(r0 + 2), q1 = load_raw(r0 + 3), q2 = load_raw(r0 + 4);
-            int i = 0;
-            for (; i + 3 <= n_rows; i += 3) {
-                step(simple_tag, ra, rb, rc, i);
-                ra = unpack(q0);
-                q0 = load_raw(r0 + i + 5);
-                step(simple_tag, rb, rc, ra, i + 1);
-                rb = unpack(q1);
-                q1 = load_raw(r0 + i + 6);
-                step(simple_tag, rc, ra, rb, i + 2);
-                rc = unpack(q2);
-                q2 = load_raw(r0 + i + 7);
+            using E0 = std::integral_constant<int, 0>;
+            using E1 = std::integral_constant<int, 1>;
+            using E2 = std::integral_constant<int, 2>;
+            RawN<NW> q0, q1, q2;
+            q0.h = q1.h = q2.h = 0u;
+            load_ptr(row_ptr(r0 - 1), r0 - 1, q0);
+            load_ptr(row_ptr(r0), r0, q1);
+            load_ptr(row_ptr(r0 + 1), r0 + 1, q2);
+            RowN<NW> ra = unpack(simple_tag, q0), rb = unpack(simple_tag, q1), rc = unpack(simple_tag, q2);
+            load_ptr(row_ptr(r0 + 2), r0 + 2, q0);
+            load_ptr(row_ptr(r0 + 3), r0 + 3, q1);
+            load_ptr(row_ptr(r0 + 4), r0 + 4, q2);
+            if (n_rows == 1) {  // a one-row band (image remainder): never a cell row
+                step(simple_tag, E0{}, ra, rb, rc, 0, false);
+                return;
             }
-            if (i < n_rows) {  // 1 or 2 remaining rows
-                step(simple_tag, ra, rb, rc, i);
-                if (i + 1 < n_rows) step(simple_tag, rb, rc, unpack(q0), i + 1);
+            step(simple_tag, E1{}, ra, rb, rc, 0, clamp_top);
+            ra = unpack(simple_tag, q0);
+            load_ptr(row_ptr(r0 + 5), r0 + 5, q0);
+            // rows in registers: rb = i-1, rc = i, ra = i+1; in flight q1, q2, q0 = i+2, i+3, i+4.
+            // The unrolled loop loads rows i+5 .. i+7 unclamped, so it stops
+            // before they pass row_hi; the tail clamps.
+            const uint8_t* ld = row_ptr(r0 + 5);
+            const int i_end = min(n_rows - 1, row_hi - r0 - 4);
+            int i = 1;
+            for (; i + 3 <= i_end; i += 3) {
+                step(simple_tag, E0{}, rb, rc, ra, i, false);
+                rb = unpack(simple_tag, q1);
+                ld += pitch;
+                load_ptr(ld, r0 + i + 5, q1);
+                step(simple_tag, E0{}, rc, ra, rb, i + 1, false);
+                rc = unpack(simple_tag, q2);
+                ld += pitch;
+                load_ptr(ld, r0 + i + 6, q2);
+                step(simple_tag, E0{}, ra, rb, rc, i + 2, false);
+                ra = unpack(simple_tag, q0);
+                ld += pitch;
+                load_ptr(ld, r0 + i + 7, q0);
             }
+            for (; i < n_rows - 1; ++i) {  // the rows before the last the loop left
+                step(simple_tag, E0{}, rb, rc, ra, i, false);
+                rb = rc;
+                rc = ra;
+                ra = unpack(simple_tag, q1);
+                q1 = q2;
+                q2 = q0;
+                load_ptr(row_ptr(r0 + i + 5), r0 + i + 5, q0);
+            }
+            step(simple_tag, E2{}, rb, rc, ra, n_rows - 1, clamp_bot);
         };
         if (ALDP_SIMPLE && simple) run_rows(std::integral_constant<bool, true>{});
         else run_rows(std::integral_constant<bool, false>{});
@@ -578,7 +665,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
             const int nb = fix_n[warp][seg];
             const int runs_per_col = nb ? max(1, (2 * SEG) / nb) : 1;
             const int run_len = nb ? (seg_rows + runs_per_col - 1) / runs_per_col : 0;
-            const int x_lo = r0, x_hi = r0 + p.cell_rows - 1;
+            const int x_lo = cell_r0, x_hi = cell_r0 + p.cell_rows - 1;
             int xs[2], len[2];
             uint32_t wsel[2], addr[2];
             const uint8_t* colp[2];
@@ -598,7 +685,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
                 // left border: (c, c, r); right border: (l, c, c)
                 const uint32_t o = uint32_t(col - 1 - wo);
                 wsel[h] = left ? (o + 1) | ((o + 1) << 4) | ((o + 2) << 8) : o | ((o + 1) << 4) | ((o + 1) << 8);
-                addr[h] = act ? seg_base + uint32_t(cc - cell_c0) * REGION + CNT : trash;
+                addr[h] = act ? seg_base + uint32_t(cc - cell_c0) * REGION + CNT + slot_skew(seg, cc - cell_c0) * 4 : trash;
             }
             int n_it = max(len[0], len[1]);
             for (int o = 16; o > 0; o >>= 1) n_it = max(n_it, __shfl_xor_sync(FULL, n_it, o));
@@ -639,9 +726,9 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
                 constexpr uint32_t M = (NT - 1) * 4;
                 uint32_t X;
                 if constexpr (LBP) X = pair_lbp(wa, wb, wc, one);
-                else X = pair_id<K>(wa, wb, wc, one);
-                red_shared(((X * 4u) & M) | (it < len[0] ? addr[0] : trash));
-                red_shared(((LBP ? X >> 6 : __umulhi(X, 1u << 18)) & M) | (it < len[1] ? addr[1] : trash));
+                else X = pair_id<K, TS>(wa, wb, wc, one);
+                red_shared(((X * 4u) & M) ^ (it < len[0] ? addr[0] : trash));
+                red_shared(((LBP ? X >> 6 : __umulhi(X, 1u << 18)) & M) ^ (it < len[1] ? addr[1] : trash));
                 wa = wb;
                 wb = wc;
             }
@@ -662,14 +749,14 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
             const int64_t cells_per_image = CELLS ? int64_t(p.grid_r) * p.grid_c : 1;
             uint8_t* seg_ptr = smem_al + (seg_base - smem_base);
             for (int j = sl; j < ntab * NT; j += SEG) {
-                const int lc = j / NT, id = j % NT;
+                const int lc = j / NT, wi = j % NT, id = wi ^ int(slot_skew(seg, lc));
                 uint32_t* cnt = reinterpret_cast<uint32_t*>(seg_ptr + lc * REGION + CNT);
-                const uint32_t v = cnt[id];
+                const uint32_t v = cnt[wi];
                 if (v) {
-                    const int64_t cell = CELLS ? int64_t(band) * p.grid_c + cell_c0 + lc : 0;
+                    const int64_t cell = CELLS ? int64_t(crow) * p.grid_c + cell_c0 + lc : 0;
                     const int bin = LBP ? id : id_bin[id];
                     atomicAdd(p.hist + (int64_t(img) * cells_per_image + cell) * p.nbins + bin, v);
-                    cnt[id] = 0;
+                    cnt[wi] = 0;
                 }
             }
             // the trash region collects masked counts: clear it too

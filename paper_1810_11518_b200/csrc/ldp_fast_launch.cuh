@@ -26,9 +26,8 @@ inline aldp_status fast_cuda_fail(cudaError_t e, const char* what) {
 template <int K, int NW, bool CELLS, bool CODES, bool HIST, bool HALO>
 aldp_status launch_fast_t(const FastParams& p, cudaStream_t st) {
     auto kern = ldp_fast_kernel<K, NW, CELLS, CODES, HIST, HALO>;
-    constexpr int NSEG = 32 / (kTileCols / (4 * NW));
-    constexpr int REGION = (K == 0 || K == 4) ? 1024 : kRegion;  // LBP: 256 counts, k == 4: 7-bit ids
-    const size_t smem = size_t(kFastWarps) * NSEG * kSegRegions * REGION + REGION;  // + alignment slack
+    constexpr int NSEG = FastLayout<K, NW>::NSEG;
+    const size_t smem = FastLayout<K, NW>::BYTES;
     // The shared-memory opt-in is a per-device function attribute: set it once
     // per device this process launches on (several GPUs in one process work).
     constexpr int kMaxDev = 64;

@@ -319,12 +319,13 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
         // Only for small batches (under kSplitTiles tiles per warp segment):
         // the remainder launch recomputes ~1 % of the pixels, more than the
         // imbalance costs a large batch (C5: -0.5 % split, C2: +4.7 %).
+        // (validate() guarantees grid_r >= 1 here: cell_rows <= rows.)
         constexpr int64_t kSplitTiles = 64;
         const int grid_rows = grid_r * a->cell_rows;
         const int64_t tiles = int64_t(a->n_images) * ((a->rows + a->cell_rows - 1) / std::max(a->cell_rows, 1)) *
                               ((a->cols + kTileCols - 1) / kTileCols);
         const int64_t seg_slots = int64_t(n_sms()) * 2 * kFastWarps * 2;
-        if (a->cell_rows && grid_r >= 1 && !a->cell_from_map && grid_rows < a->rows && tiles < kSplitTiles * seg_slots) {
+        if (a->cell_rows && !a->cell_from_map && grid_rows < a->rows && tiles < kSplitTiles * seg_slots) {
             FastParams q = p;
             p.rows = grid_rows;
             p.row_hi = grid_rows - 1;
