@@ -10,8 +10,9 @@ F="-gencode arch=compute_100a,code=sm_100a -lineinfo -O3 -std=c++20 -Xcompiler -
 for s in ldp_kernels.cu ldp_fast_cells.cu ldp_host.cu ldp_field.cu aldp_api.cpp aldp_io.cpp; do
   X=""; [ "$s" == "ldp_fast_cells.cu" ] && X="${CELLS_FLAGS--Xptxas --register-usage-level=10}"
   nvcc $F $X "$@" -c -o variants/obj_$NAME/$s.o paper_1810_11518_b200/csrc/$s &
+  pids="$pids $!"
 done
-wait
+for p in $pids; do wait $p || { echo "variant $NAME: compile failed" >&2; exit 1; }; done
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o variants/libaldp_$NAME.so variants/obj_$NAME/*.o
 rm -rf variants/obj_$NAME
 echo variants/libaldp_$NAME.so
