@@ -90,6 +90,11 @@ typedef struct {
      * copy, so a tall frame can be processed as bands with identical codes
      * and histograms (cells must then start at a multiple of cell_rows). */
     int rows_above, rows_below;
+    /* 1: d_hist holds uint16 counts, [n_images][grid_cells][bins] (4-byte
+     * aligned; every bin count is even), for a compact multi-GPU gather. Valid
+     * only while no histogram can reach 65536 (cell area, or rows * cols for
+     * whole-image histograms, below 65536) -> ALDP_EINVAL otherwise. */
+    int hist_u16;
 } aldp_ldp_args;
 
 aldp_status aldp_ldp_batch(const aldp_ldp_args* args, void* stream);
@@ -109,6 +114,17 @@ aldp_status aldp_ldp_batch_ex(const aldp_ldp_args* args, int kernel, void* strea
  * d_hist is uint32 [n_images][grid_cells][256]. Same border and cell rules. */
 aldp_status aldp_lbp_batch(const aldp_ldp_args* args, void* stream);
 aldp_status aldp_lbp_batch_ex(const aldp_ldp_args* args, int kernel, void* stream);
+
+/* Kernel launches the last aldp_ldp_batch* / aldp_lbp_batch* call on this
+ * host thread made (0, 1, or 2 for a cell grid whose rows overhang it). */
+int aldp_last_launch_count(void);
+
+/* Negative control for parity harnesses (the analogue of the reference's
+ * FaultInjection, include/aldp/verify.hpp:14-20): while mode is 1, every
+ * batch launch flips bit 0 of image 0's code at (0, 0) and adds one count to
+ * bin 0 of image 0's first histogram. 0 turns it off. The environment
+ * variable ALDP_FAULT_INJECT sets the initial mode. Returns the old mode. */
+int aldp_debug_fault(int mode);
 
 /* Number of histogram bins for k: C(8, k) (56 for k == 3), 0 if k invalid. */
 int aldp_n_bins(int k);
@@ -156,6 +172,37 @@ aldp_status aldp_lbp_batch_host(const uint8_t* pixels, int n_images, int rows, i
 aldp_status aldp_ldp_batch_host(const uint8_t* pixels, int n_images, int rows, int cols, int k,
                                 int cell_rows, int cell_cols, uint8_t* codes, uint32_t* hist,
                                 void* stream);
+
+/* ---- several GPUs in one process ----
+ * aldp_ldp_batch_host over n_devices GPUs: the images are split into
+ * contiguous ranges, one per entry of `devices` (NULL: every visible device,
+ * n_devices ignored), and each range runs the chunked H2D / kernel / D2H
+ * pipeline of aldp_ldp_batch_host on its device from its own persistent host
+ * worker thread (its pinned staging and streams are reused across calls).
+ * Images are independent, so there is no collective: each device copies its
+ * codes and histograms straight into its slice of the caller's buffers.
+ * Results are identical for any device list (a device may repeat). The
+ * reference's only concurrency is the same fan-out over image ranges, on CPU
+ * threads (proj/src/verify.cpp:85-98). Blocks until every range is done. */
+aldp_status aldp_ldp_batch_host_multi(const uint8_t* pixels, int n_images, int rows, int cols, int k,
+                                      int cell_rows, int cell_cols, uint8_t* codes, uint32_t* hist,
+                                      const int* devices, int n_devices);
+aldp_status aldp_lbp_batch_host_multi(const uint8_t* pixels, int n_images, int rows, int cols, int cell_rows,
+                                      int cell_cols, uint8_t* codes, uint32_t* hist, const int* devices,
+                                      int n_devices);
+
+/* Device-resident batches on several GPUs: args[i] (device pointers on
+ * devices[i]) is launched on devices[i], stream streams[i] (NULL entries or
+ * NULL array: the legacy default stream), all asynchronously; the calling
+ * thread's current device is restored. */
+aldp_status aldp_ldp_batch_multi(const aldp_ldp_args* args, const int* devices, void* const* streams, int n);
+
+/* Gathers n device buffers into one buffer on dst_device, back to back in
+ * order (srcs[i], bytes[i] on src_devices[i]), with peer copies over NVLink
+ * (cudaMemcpyPeerAsync) ordered on `stream` (a stream of dst_device). Used
+ * for the per-image histogram gather to one GPU. */
+aldp_status aldp_gather_peer(void* dst, int dst_device, const void* const* srcs, const int* src_devices,
+                             const size_t* bytes, int n, void* stream);
 
 /* ---- response field and the equivalence sweep ---- */
 

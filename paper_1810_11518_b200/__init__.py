@@ -38,7 +38,7 @@ __all__ = [
     "lbp_histogram", "lbp_code_map", "lbp_batch", "response_field", "response_field_batch",
     "FaultInjection", "Mismatch", "VerifyResult", "verify_equivalence", "verify_image", "verify_batch",
     "PgmError", "load_pgm", "save_pgm", "load_pgm_batch", "extract_files", "op_counts", "bench_csv",
-    "CLI_PATH",
+    "CLI_PATH", "last_launch_count", "debug_fault", "ldp_batch_host_multi",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -90,6 +90,7 @@ class _Args(ctypes.Structure):
         ("d_codes", ctypes.c_void_p), ("codes_img_stride", ctypes.c_int64),
         ("codes_pitch", ctypes.c_int), ("d_hist", ctypes.c_void_p),
         ("cell_from_map", ctypes.c_int), ("rows_above", ctypes.c_int), ("rows_below", ctypes.c_int),
+        ("hist_u16", ctypes.c_int),
     ]
 
 
@@ -127,7 +128,13 @@ def _load() -> ctypes.CDLL:
         "aldp_lbp_histogram": ([P, I, I, P], I),
         "aldp_lbp_code_map": ([P, I, I, P], I),
         "aldp_lbp_batch_host": ([P, I, I, I, I, I, P, P, P], I),
+        "aldp_ldp_batch_host_multi": ([P, I, I, I, I, I, I, P, P, P, I], I),
+        "aldp_lbp_batch_host_multi": ([P, I, I, I, I, I, P, P, P, I], I),
+        "aldp_ldp_batch_multi": ([ctypes.POINTER(_Args), P, P, I], I),
+        "aldp_gather_peer": ([P, I, P, P, P, I, P], I),
         "aldp_last_error": ([], ctypes.c_char_p),
+        "aldp_last_launch_count": ([], I),
+        "aldp_debug_fault": ([I], I),
         "aldp_gen_faces": ([P, I, I, I, I, I64, I, U64, I64, P], I),
         "aldp_gen_ties": ([P, I, I, I, I, I64, U64, I64, P], I),
         "aldp_version": ([], ctypes.c_char_p),
@@ -293,6 +300,36 @@ def ldp_batch_host(pixels: np.ndarray, k: int = 3, cell: Tuple[int, int] = (0, 0
     return c, h
 
 
+def ldp_batch_host_multi(pixels: np.ndarray, k: int = 3, cell: Tuple[int, int] = (0, 0),
+                         codes: bool = True, hist: bool = True, devices=None):
+    """ldp_batch_host over several GPUs of this process
+    (aldp_ldp_batch_host_multi): contiguous image ranges, one per entry of
+    `devices` (None: every visible device), each on its own persistent host
+    worker. Same results as ldp_batch_host for any device list. k == 0: LBP."""
+    px = np.ascontiguousarray(pixels, dtype=np.uint8)
+    if px.ndim == 2:
+        px = px[None]
+    n, rows, cols = px.shape
+    nb = 256 if k == 0 else n_bins(k)
+    cells = grid_cells(rows, cols, *cell)
+    c = np.empty_like(px) if codes else None
+    h = np.empty((n, cells, nb), dtype=np.uint32) if hist else None
+    cp = c.ctypes.data if c is not None else None
+    hp = h.ctypes.data if h is not None else None
+    if devices is None:
+        dp, nd = None, 0
+    else:
+        dv = (ctypes.c_int * len(devices))(*[int(d) for d in devices])
+        dp, nd = ctypes.cast(dv, ctypes.c_void_p), len(devices)
+    if k == 0:
+        _check(lib.aldp_lbp_batch_host_multi(px.ctypes.data, n, rows, cols, int(cell[0]), int(cell[1]), cp, hp,
+                                             dp, nd))
+    else:
+        _check(lib.aldp_ldp_batch_host_multi(px.ctypes.data, n, rows, cols, int(k), int(cell[0]), int(cell[1]),
+                                             cp, hp, dp, nd))
+    return c, h
+
+
 _KERNEL = {"auto": 0, "fast": 1, "generic": 2}
 
 
@@ -310,7 +347,9 @@ def ldp_batch(pixels, rows: int, cols: int, k: int = 3, cell: Tuple[int, int] = 
 
     pixels: torch.uint8 CUDA tensor [n, rows, pitch] (contiguous; pitch >= cols).
     codes:  None, True (allocate) or a torch.uint8 tensor [n, rows, codes_pitch].
-    hist:   None, True (allocate) or a torch.int32/uint32 tensor [n, cells, n_bins].
+    hist:   None, True (allocate) or a torch.int32/uint32 tensor [n, cells, n_bins];
+            a torch.int16/uint16 tensor gets uint16 counts (the compact
+            multi-GPU wire; every histogram must stay below 65536 counts).
     stream: a raw cudaStream_t (int); default: torch's current stream.
     cell_clamp: True (the reference's windowed_features rule) clamps every
             cell as its own image; False cuts cells from the whole-image code
@@ -352,8 +391,9 @@ def ldp_batch(pixels, rows: int, cols: int, k: int = 3, cell: Tuple[int, int] = 
         a.codes_pitch = codes.shape[2]
         a.codes_img_stride = codes.shape[1] * codes.shape[2]
     if hist is not None:
-        if hist.dtype not in (torch.int32, torch.uint32):
-            raise ValueError(f"hist must be int32 or uint32, got {hist.dtype}")
+        if hist.dtype not in (torch.int32, torch.uint32, torch.int16, torch.uint16):
+            raise ValueError(f"hist must be int32/uint32 (or int16/uint16), got {hist.dtype}")
+        a.hist_u16 = int(hist.dtype in (torch.int16, torch.uint16))
         if hist.device != pixels.device:
             raise ValueError(f"hist is on {hist.device}, pixels on {pixels.device}")
         if hist.numel() < n * cells * nb or not hist.is_contiguous():
@@ -364,6 +404,18 @@ def ldp_batch(pixels, rows: int, cols: int, k: int = 3, cell: Tuple[int, int] = 
     fn = lib.aldp_lbp_batch_ex if k == 0 else lib.aldp_ldp_batch_ex
     _check(fn(ctypes.byref(a), _KERNEL[kernel], stream or None))
     return codes, hist
+
+
+def last_launch_count() -> int:
+    """Kernels the last ldp_batch / lbp_batch call on this thread launched."""
+    return int(lib.aldp_last_launch_count())
+
+
+def debug_fault(mode: int) -> int:
+    """Negative control (aldp_debug_fault): while mode is 1 every batch flips
+    image 0's first code bit and adds a count to its first bin. Returns the
+    previous mode."""
+    return int(lib.aldp_debug_fault(int(mode)))
 
 
 def _pitch(cols: int, pitch: Optional[int]) -> int:

@@ -78,6 +78,8 @@ struct FastParams {
     int codes_pitch;
     uint32_t* hist;
     int nbins;
+    int hist16;  // hist holds uint16 counts (two bins per 32-bit word)
+    int fault;   // aldp_debug_fault: corrupt image 0's first code and bin
     int cell_rows, cell_cols, grid_r, grid_c;  // cell mode only
     int cell_clamp;                            // cell mode: 1 = per-cell clamp, 0 = cut from the code map
     int edge_lo, edge_hi;                      // band rows recounted with the cell clamp (-1: none)
@@ -96,6 +98,13 @@ struct FastParams {
 // Tag set of a fast-kernel instantiation (ldp_common.cuh kTagT): the cell
 // kernel keeps set 0, the whole-image kernel takes set 1.
 __host__ __device__ constexpr int fast_tag_set(bool cells) { return cells ? 0 : 1; }
+
+// hist[idx] += v on uint32 counts, or on uint16 counts packed two per word
+// (a count never reaches 65536 there, so the add cannot carry across bins)
+__device__ __forceinline__ void hist_add(uint32_t* hist, int hist16, int64_t idx, uint32_t v) {
+    if (hist16) atomicAdd(hist + (idx >> 1), v << (16 * int(idx & 1)));
+    else atomicAdd(hist + idx, v);
+}
 
 __device__ __forceinline__ uint32_t fdiv(uint32_t n, uint64_t m, int sh) {
     return uint32_t((uint64_t(n) * m) >> sh);
@@ -755,13 +764,17 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
                 if (v) {
                     const int64_t cell = CELLS ? int64_t(crow) * p.grid_c + cell_c0 + lc : 0;
                     const int bin = LBP ? id : id_bin[id];
-                    atomicAdd(p.hist + (int64_t(img) * cells_per_image + cell) * p.nbins + bin, v);
+                    hist_add(p.hist, p.hist16, (int64_t(img) * cells_per_image + cell) * p.nbins + bin, v);
                     cnt[wi] = 0;
                 }
             }
             // the trash region collects masked counts: clear it too
             uint32_t* tr = reinterpret_cast<uint32_t*>(seg_ptr + kMaxTileCells * REGION + CNT);
             for (int j = sl; j < NT; j += SEG) tr[j] = 0;
+        }
+        if (p.fault && seg_live && img == 0 && r0 == 0 && blk == 0 && sl == 0) {  // negative control
+            if (CODES) p.codes[0] ^= 1;
+            if (HIST && do_hist) hist_add(p.hist, p.hist16, 0, 1u);
         }
         __syncwarp();
     }

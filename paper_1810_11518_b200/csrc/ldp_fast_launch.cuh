@@ -18,6 +18,7 @@ namespace aldp_b200 {
 
 aldp_status set_error(aldp_status s, const std::string& msg);  // ldp_kernels.cu
 int fast_n_sms();                                               // ldp_kernels.cu
+void count_launch();                                            // ldp_kernels.cu (aldp_last_launch_count)
 
 inline aldp_status fast_cuda_fail(cudaError_t e, const char* what) {
     return set_error(ALDP_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -50,6 +51,7 @@ aldp_status launch_fast_t(const FastParams& p, cudaStream_t st) {
     const int64_t want = (warp_tiles + kFastWarps - 1) / kFastWarps;
     const int grid = int(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(per_sm) * fast_n_sms())));
     kern<<<grid, kFastWarps * 32, smem, st>>>(p);
+    count_launch();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fast_cuda_fail(e, "ldp_fast_kernel launch");
     return ALDP_OK;

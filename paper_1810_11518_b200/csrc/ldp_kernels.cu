@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -34,6 +35,13 @@ namespace aldp_b200 {
 // error plumbing
 // --------------------------------------------------------------------------
 static thread_local std::string t_last_error;
+static thread_local int t_launches;  // kernels the last batch call launched (aldp_last_launch_count)
+// aldp_debug_fault mode; ALDP_FAULT_INJECT sets the initial value
+static std::atomic<int> g_fault{[] {
+    const char* e = std::getenv("ALDP_FAULT_INJECT");
+    return e ? std::atoi(e) : 0;
+}()};
+void count_launch() { ++t_launches; }
 
 // Records `msg` as this host thread's last error (aldp_last_error) and
 // returns `s`. Shared with ldp_host.cu.
@@ -55,6 +63,14 @@ static aldp_status cuda_fail(cudaError_t e, const char* what) {
     } while (0)
 
 // --------------------------------------------------------------------------
+// fast kernel (ldp_fast.cuh)
+// --------------------------------------------------------------------------
+}  // namespace aldp_b200
+#include "ldp_fast.cuh"
+#include "ldp_fast_launch.cuh"
+namespace aldp_b200 {
+
+// --------------------------------------------------------------------------
 // generic kernel: one thread per pixel
 // --------------------------------------------------------------------------
 struct GenericParams {
@@ -66,6 +82,8 @@ struct GenericParams {
     int codes_pitch;
     uint32_t* hist;
     int nbins;
+    int hist16;                                // uint16 counts, two per word
+    int fault;                                 // aldp_debug_fault
     int cell_rows, cell_cols, grid_r, grid_c;  // cell_rows == 0: whole image
     int cell_clamp;                            // 0: cells cut from the whole-image code map
     int row_lo, row_hi;                        // neighbour rows readable (halo rows of a band view)
@@ -83,11 +101,13 @@ __global__ void ldp_generic_kernel(GenericParams p) {
         // k == 0: LBP (256 bins indexed by the code itself)
         const unsigned code = p.k ? clamped_code(base, p.pitch, x, y, p.row_lo, p.row_hi, 0, p.cols - 1, p.k)
                                   : clamped_lbp(base, p.pitch, x, y, p.row_lo, p.row_hi, 0, p.cols - 1);
+        const bool fault = p.fault && t == 0;  // negative control: image 0, pixel (0, 0)
         if (p.codes)
-            p.codes[img * p.codes_img_stride + int64_t(x) * p.codes_pitch + y] = uint8_t(code);
+            p.codes[img * p.codes_img_stride + int64_t(x) * p.codes_pitch + y] = uint8_t(code ^ (fault ? 1u : 0u));
         if (!p.hist) continue;
+        if (fault) hist_add(p.hist, p.hist16, 0, 1u);
         if (p.cell_rows == 0) {
-            atomicAdd(p.hist + int64_t(img) * p.nbins + (p.k ? colex_rank(code) : code), 1u);
+            hist_add(p.hist, p.hist16, int64_t(img) * p.nbins + (p.k ? colex_rank(code) : code), 1u);
         } else {
             const int cr = x / p.cell_rows, cc = y / p.cell_cols;
             if (cr >= p.grid_r || cc >= p.grid_c) continue;  // remainder dropped
@@ -99,18 +119,11 @@ __global__ void ldp_generic_kernel(GenericParams p) {
                 hc = p.k ? clamped_code(base, p.pitch, x, y, x0, x0 + p.cell_rows - 1, y0, y0 + p.cell_cols - 1, p.k)
                          : clamped_lbp(base, p.pitch, x, y, x0, x0 + p.cell_rows - 1, y0, y0 + p.cell_cols - 1);
             const int64_t cell = int64_t(img) * p.grid_r * p.grid_c + int64_t(cr) * p.grid_c + cc;
-            atomicAdd(p.hist + cell * p.nbins + (p.k ? colex_rank(hc) : hc), 1u);
+            hist_add(p.hist, p.hist16, cell * p.nbins + (p.k ? colex_rank(hc) : hc), 1u);
         }
     }
 }
 
-// --------------------------------------------------------------------------
-// fast kernel (ldp_fast.cuh)
-// --------------------------------------------------------------------------
-}  // namespace aldp_b200
-#include "ldp_fast.cuh"
-#include "ldp_fast_launch.cuh"
-namespace aldp_b200 {
 
 // --------------------------------------------------------------------------
 // dispatch
@@ -260,15 +273,22 @@ static aldp_status finish_fast(FastParams& p, int n_images, int cell_rows, int c
 
 // lbp: the LBP descriptor (256 bins, k ignored); internally k == 0.
 static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st, bool lbp) {
+    t_launches = 0;
     int grid_r = 1, grid_c = 1;
     aldp_status s = validate(a, &grid_r, &grid_c, lbp);
     if (s != ALDP_OK) return s;
     const int k = lbp ? 0 : a->k;
     const int nbins = lbp ? 256 : aldp_n_bins(a->k);
     const int64_t cells = a->cell_rows ? int64_t(grid_r) * grid_c : 1;
+    if (a->hist_u16) {
+        const int64_t area = a->cell_rows ? int64_t(a->cell_rows) * a->cell_cols : int64_t(a->rows) * a->cols;
+        if (area >= 65536) return fail(ALDP_EINVAL, "hist_u16: a histogram can reach 65536 counts");
+        if (reinterpret_cast<uintptr_t>(a->d_hist) % 4) return fail(ALDP_EINVAL, "hist_u16: d_hist not 4-byte aligned");
+    }
+    const int fault = g_fault.load(std::memory_order_relaxed);
     if (a->d_hist)
         ALDP_CUDA_TRY(cudaMemsetAsync(a->d_hist, 0,
-                                      sizeof(uint32_t) * size_t(a->n_images) * cells * nbins, st));
+                                      (a->hist_u16 ? 2 : 4) * size_t(a->n_images) * cells * nbins, st));
     if (a->n_images == 0 || (!a->d_codes && !a->d_hist)) return ALDP_OK;
 
     const int al = 4 * kLaneWords;  // alignment the per-lane vector loads/stores need
@@ -296,6 +316,8 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
         p.codes_pitch = a->codes_pitch;
         p.hist = a->d_hist;
         p.nbins = nbins;
+        p.hist16 = a->hist_u16 ? 1 : 0;
+        p.fault = fault;
         p.cell_rows = a->cell_rows;
         p.cell_cols = a->cell_cols;
         p.cell_clamp = a->cell_from_map ? 0 : 1;
@@ -339,6 +361,7 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
             q.rows = a->rows - start;
             q.codes = a->d_codes + int64_t(start) * a->codes_pitch;
             q.hist = nullptr;
+            q.fault = 0;
             q.cell_rows = q.cell_cols = 0;
             q.grid_r = q.grid_c = 1;
             q.edge_lo = q.edge_hi = -1;
@@ -362,6 +385,8 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
     g.codes_pitch = a->codes_pitch;
     g.hist = a->d_hist;
     g.nbins = nbins;
+    g.hist16 = a->hist_u16 ? 1 : 0;
+    g.fault = fault;
     g.cell_rows = a->cell_rows;
     g.cell_cols = a->cell_cols;
     g.cell_clamp = a->cell_from_map ? 0 : 1;
@@ -372,6 +397,7 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
     const int64_t total = int64_t(a->rows) * a->cols * a->n_images;
     const int grid = int(std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 32LL * n_sms())));
     ldp_generic_kernel<<<grid, 256, 0, st>>>(g);
+    count_launch();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "ldp_generic_kernel launch");
     return ALDP_OK;
@@ -415,6 +441,10 @@ int64_t aldp_grid_cells(int rows, int cols, int cell_rows, int cell_cols) {
 }
 
 const char* aldp_last_error(void) { return t_last_error.c_str(); }
+
+int aldp_last_launch_count(void) { return t_launches; }
+
+int aldp_debug_fault(int mode) { return g_fault.exchange(mode); }
 
 const char* aldp_version(void) { return "aldp_b200 0.1.0 sm_100a"; }
 
