@@ -124,15 +124,37 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(sm)}
 
 
-def ncu_traffic_bpp():
-    """DRAM bytes/pixel of the fast kernel from the last committed ncu --set
-    full capture (profiles/traffic.json), or None."""
+def ncu_record(cfg):
+    """Limiter counters of the fast kernel for this config from the ncu
+    --set full capture recorded in profiles/ncu_metrics.json (tools/ncu_to_json.py),
+    and whether that capture ran the library loaded now (sha256)."""
+    import hashlib
     try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            d = json.load(f)
-        return float(d["dram_bytes_per_pixel"]), d.get("source", "")
-    except (OSError, KeyError, ValueError):
-        return None, None
+        with open(os.path.join(ROOT, "profiles", "ncu_metrics.json")) as f:
+            rec = json.load(f).get(cfg)
+    except (OSError, ValueError):
+        return None
+    if not rec:
+        return None
+    import paper_1810_11518_b200 as aldp
+    try:
+        sha = hashlib.sha256(open(aldp.LIB_PATH, "rb").read()).hexdigest()
+    except OSError:
+        sha = None
+    rec = dict(rec)
+    rec["same_build"] = sha is not None and sha == rec.get("lib_sha256")
+    return rec
+
+
+def limiter_of(rec):
+    """Name the measured limiter from the ncu counters: the unit closest to
+    its peak among DRAM, the L1/shared data pipe, the ALU pipe and instruction
+    issue."""
+    if not rec:
+        return None
+    units = {"dram": rec.get("dram_throughput_pct", 0.0), "l1_data_pipe": rec.get("l1_data_pipe_pct", 0.0),
+             "alu_pipe": rec.get("alu_pipe_pct", 0.0), "issue": rec.get("issue_active_pct", 0.0)}
+    return max(units, key=units.get)
 
 
 def measured_peaks():
@@ -171,6 +193,25 @@ def numpy_faces(n, rows, cols, blobs, seed):
     return out
 
 
+def device_inputs(gen, n, rows, cols, blobs, seed, rows_kept=None):
+    """The B200 arm's synthetic inputs (device generator keyed by image index
+    from 0), copied back to the host: [n, rows_kept, cols] uint8."""
+    import torch
+    import paper_1810_11518_b200 as aldp
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
+    if gen == "faces":
+        d = aldp.gen_faces(n, rows, cols, blobs=blobs, seed=seed, pitch=cols, device=dev)
+    elif gen == "ties":
+        d = aldp.gen_ties(n, rows, cols, seed=seed, pitch=cols, device=dev)
+    else:
+        raise ValueError(gen)
+    torch.cuda.synchronize(dev)
+    out = d[:, :rows_kept or rows, :cols].cpu().numpy()
+    del d
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_reference(args, cfg_name):
     """--impl reference: the reference's CPU implementation (oracle/_ref)."""
     import numpy as np
@@ -185,19 +226,30 @@ def run_reference(args, cfg_name):
     threads = os.cpu_count() or 1
     sample = max(threads * 4, 32) if cfg_name in ("c5", "c2", "c5w", "c5lbp") else \
         (threads if cfg_name == "c3" else 1)
-    if gen == "faces" and rows * cols >= 1e8:
+    # Inputs: the product arm's own bytes -- the device generator's output for
+    # images 0 .. sample-1 (or C4's first 1024 rows), copied back before any
+    # timing; only the reference library runs in the timed loop.
+    src = "device generator bytes (same as the B200 arm), copied to the host untimed"
+    try:
+        px = device_inputs(gen, sample if rows * cols < 1e8 else 1, rows, cols, blobs, seed,
+                           rows_kept=1024 if rows * cols >= 1e8 else rows)
+    except Exception as e:  # noqa: BLE001 -- no GPU: the numpy restatement of the recipe
+        src = f"numpy restatement of the generator ({type(e).__name__}: no device)"
+        px = None
+    if gen == "random":
+        px = oracle.ref_make_random(rows, cols, seed)[None]  # the reference's own generator
+        src = "reference make_random (mt19937)"
+    elif px is None and gen == "faces":
+        px = numpy_faces(sample if rows * cols < 1e8 else 1, rows if rows * cols < 1e8 else 1024, cols,
+                         blobs if rows * cols < 1e8 else max(1, blobs // 16), seed)
+    elif px is None:
+        px = np.random.default_rng(seed).integers(0, 3, size=(sample, rows, cols), dtype=np.uint8)
+    if rows * cols >= 1e8:
         # C4: a band of the 16384^2 frame (1024 rows), cut into one row band of
         # whole 64-row cells per host thread -- cells are clamped independently,
         # so the bands are exactly the frame's work for those rows
-        band = numpy_faces(1, 1024, cols, max(1, blobs // 16), seed)[0]
-        px = band.reshape(1024 // cr, cr, cols) if cr else band[None]
-    elif gen == "faces":
-        px = numpy_faces(sample, rows, cols, blobs, seed)
-    elif gen == "ties":
-        rng = np.random.default_rng(seed)
-        px = rng.integers(0, 3, size=(sample, rows, cols), dtype=np.uint8)
-    else:
-        px = oracle.ref_make_random(rows, cols, seed)[None]
+        band = px[0]
+        px = band.reshape(band.shape[0] // cr, cr, cols) if cr else band[None]
     kind = "reference" if oracle.have_ref() else "port"
     run = (lambda: oracle.ref_batch(px, k=k, cell=(cr, cc), threads=threads)) if kind == "reference" \
         else (lambda: oracle.batch(px, k=k, cell=(cr, cc), threads=threads))
@@ -213,7 +265,7 @@ def run_reference(args, cfg_name):
         "value": round(mpx, 3),
         "unit": "Mpixel/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "u8", "data": "synthetic (numpy face-like, same recipe)",
+        "vs_baseline": None, "dtype": "u8", "data": f"synthetic: {src}",
         "config": {"workload": workload_name(cfg_name, k), "images_per_step": int(px.shape[0]),
                    "parallelism": f"{threads} host threads over images", "cpu_only": True},
         "cpu_baseline": {"value": round(mpx, 3), "unit": "Mpixel/s", "cores": threads, "kind": kind,
@@ -261,15 +313,21 @@ def cpu_baseline(host_px, k, cr, cc):
     kind = "reference" if oracle.have_ref() else "port"
     res = {}
     n = host_px.shape[0]
-    for label, path, nthreads, count in (("aldp_all_cores", 1, threads, n), ("ldp_all_cores", 0, threads, n // 2),
-                                         ("aldp_1_thread", 1, 1, max(1, n // threads)),
-                                         ("ldp_1_thread", 0, 1, max(1, n // threads // 2))):
+    # *_hist_only: the histograms alone (ldp_histogram / windowed_features, the
+    # reference API's one pass); the others also build the code map, which the
+    # reference only has as a second pass (no fused entry point)
+    for label, path, nthreads, count, codes in (
+            ("aldp_all_cores", 1, threads, n, True), ("ldp_all_cores", 0, threads, n // 2, True),
+            ("aldp_hist_only_all_cores", 1, threads, n, False),
+            ("aldp_1_thread", 1, 1, max(1, n // threads), True),
+            ("ldp_1_thread", 0, 1, max(1, n // threads // 2), True)):
         sub = host_px[:max(count, 1)]
         if kind == "reference":
-            dt = oracle.ref_median_seconds_batch(sub, k=k, cell=(cr, cc), path=path, threads=nthreads, repeats=3)
+            dt = oracle.ref_median_seconds_batch(sub, k=k, cell=(cr, cc), path=path, threads=nthreads, repeats=3,
+                                                 codes=codes)
         else:
             t0 = time.perf_counter()
-            oracle.batch(sub, k=k, cell=(cr, cc), threads=nthreads)
+            oracle.batch(sub, k=k, cell=(cr, cc), threads=nthreads, codes=codes)
             dt = time.perf_counter() - t0
         res[label] = round(sub.size / dt / 1e6, 3)
     return {"value": res["aldp_all_cores"], "unit": "Mpixel/s", "cores": threads, "kind": kind,
@@ -322,6 +380,13 @@ def main():
     dev = torch.device("cuda", local)
     use_dist = world > 1 or args.force_dist
     if use_dist:
+        if "RANK" not in os.environ:  # --force-dist outside torchrun: a one-rank group
+            import socket
+            sk = socket.socket()
+            sk.bind(("127.0.0.1", 0))
+            os.environ.update(RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1",
+                              MASTER_PORT=str(sk.getsockname()[1]))
+            sk.close()
         dist.init_process_group("nccl", device_id=dev)
 
     n, rows, cols, k, cr, cc, blobs, gen, seed = CONFIGS[args.config]
@@ -343,22 +408,21 @@ def main():
         elif gen == "ties":
             px = aldp.gen_ties(mine, rows, cols, seed=seed, first_index=lo, pitch=pitch, device=dev,
                                stream=sp)
-        else:
-            import oracle
-            px = torch.from_numpy(oracle.make_random(rows, cols, seed)[None].copy()).to(dev)
+        else:  # config 1: the reference's make_random (mt19937), the library's own copy
+            px = torch.from_numpy(aldp.make_random(rows, cols, seed)[None].copy()).to(dev)
         cells = aldp.grid_cells(rows, cols, cr, cc)
         nb = 256 if k == 0 else aldp.n_bins(k)
         codes = torch.empty((mine, rows, pitch), dtype=torch.uint8, device=dev)
-        hist = torch.empty((mine, cells, nb), dtype=torch.int32, device=dev)
+        # With a gather (N > 1) the kernel writes uint16 counts directly (a
+        # cell holds at most 81*91 = 7371 < 65536 pixels): they are the wire.
+        wire16 = use_dist and wire_dtype_ok((cr or rows) * (cc or cols))
+        hist = torch.empty((mine, cells, nb), dtype=torch.int16 if wire16 else torch.int32, device=dev)
         gathered = None
         if use_dist:
-            # uint16 on the wire: a cell count is at most 81*91 = 7371 < 65536
-            assert wire_dtype_ok((cr or rows) * (cc or cols))
             per = [shard_range(n, r, world)[1] - shard_range(n, r, world)[0] for r in range(world)]
             assert len(set(per)) == 1, "image count must divide evenly across ranks"
-            wire = torch.empty((mine, cells, nb), dtype=torch.int16, device=dev)
             if rank == 0:
-                gathered = [torch.empty_like(wire) for _ in range(world)]
+                gathered = [torch.empty_like(hist) for _ in range(world)]
     stream.synchronize()
 
     # Chunks: with a gather (N > 1), chunk i's histograms travel on the comm
@@ -370,16 +434,21 @@ def main():
     chunk_ev = [torch.cuda.Event() for _ in bounds]
     comm_done = torch.cuda.Event()
 
+    launches = [0]  # kernels launched by the last step (the library's own count)
+
     def launch_chunks():
+        launches[0] = 0
         for ci, (a, b) in enumerate(bounds):
             aldp.ldp_batch(px[a:b], rows, cols, k=k, cell=(cr, cc), codes=codes[a:b], hist=hist[a:b],
                            kernel=args.kernel, stream=sp)
+            launches[0] += aldp.last_launch_count()
             if use_dist:
                 chunk_ev[ci].record(stream)
                 comm.wait_event(chunk_ev[ci])
                 with torch.cuda.stream(comm):
-                    gather_histograms(hist[a:b], dist, rank, world, wire=wire[a:b],
-                                      out=[g[a:b] for g in gathered] if rank == 0 else None)
+                    gather_histograms(hist[a:b], dist, rank, world,
+                                      out=[g[a:b] for g in gathered] if rank == 0 else None,
+                                      max_count=(cr or rows) * (cc or cols))
 
     def finish_step():
         if use_dist:
@@ -431,28 +500,19 @@ def main():
     w = torch.arange(1, nb + 1, device=dev, dtype=torch.int64)
     sums = torch.zeros(2, device=dev, dtype=torch.int64)
     for a in range(0, mine, 2048):  # chunked: never materialise a widened copy of 20 GB
-        sums[0] += (hist[a:a + 2048].to(torch.int64) * w).sum()
+        sums[0] += ((hist[a:a + 2048].to(torch.int64) & 0xFFFF) * w).sum()  # int16 counts are < 65536
         sums[1] += codes[a:a + 2048, :, :cols].sum(dtype=torch.int64)
     if use_dist:
         dist.all_reduce(sums)
     checks = {"hist_weighted_sum": int(sums[0]), "code_sum": int(sums[1]),
               "note": "sum over all images of bin-index-weighted counts, and of code bytes"}
 
-    # kernels per ldp_batch call: cell histograms over a frame whose rows
-    # overhang the cell grid run the grid and the remainder rows (codes only)
-    # as two launches (ldp_kernels.cu run_batch)
-    # (small batches only: under 64 tiles per warp segment, as run_batch decides)
-    seg_slots = torch.cuda.get_device_properties(dev).multi_processor_count * 2 * 8 * 2
-
-    def kernels_of(m):
-        tiles = m * (-(-rows // cr) if cr else 1) * -(-cols // 128)
-        return 2 if cr and rows % cr and tiles < 64 * seg_slots else 1
-
-    kernels_per_step = sum(kernels_of(b - a) for a, b in bounds)
+    kernels_per_step = launches[0]
 
     # ---- roofline of the dominant kernel (one launch = this rank's shard) ----
     hbm, peak_src = measured_peaks()
-    traffic_bpp, traffic_src = ncu_traffic_bpp()
+    ncu = ncu_record(args.config if k == CONFIGS[args.config][3] else f"{args.config}_k{k}")
+    traffic_bpp = ncu["dram_bytes_per_px"] if ncu else None
     bpp_hist = hist_bytes_per_image(rows, cols, k, cr, cc) / (rows * cols)
     alg_bytes = mine * rows * cols * (2.0 + bpp_hist)
     achieved = alg_bytes / (launch_ms * 1e-3) / 1e9
@@ -472,13 +532,16 @@ def main():
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                      "frac": round(achieved / hbm, 4),
                      "traffic": (round(traffic_bpp * mine * rows * cols / (launch_ms * 1e-3) / 1e9, 1)
-                                 if traffic_bpp and args.config == "c5" else None),
+                                 if traffic_bpp else None),
                      "traffic_unit": "GB/s (ncu dram bytes per pixel x pixels per launch / launch time)",
-                     "traffic_source": traffic_src,
                      "peak_source": peak_src,
                      "bytes_per_pixel": round(2.0 + bpp_hist, 4),
                      "launch_ms": round(launch_ms, 4), "launch_median_ms": round(launch_median_ms, 4),
-                     "launches_per_step": kernels_per_step},
+                     "launches_per_step": kernels_per_step,
+                     # what ncu measured for this kernel: the roofline is HBM, but
+                     # the kernel is limited by instruction issue / the ALU pipe
+                     "limiter": limiter_of(ncu),
+                     "ncu": ncu},
         "clocks": clocks,
         "gpu_launches": args.steps * kernels_per_step,
     }
@@ -521,8 +584,32 @@ def main():
                        "images_per_step": e2n * world, "ranks": world,
                        "timing": "host wall clock per rank, max over ranks",
                        "api": "aldp_ldp_batch_host (C-ABI, host buffers)"}
+        # the same call from pageable buffers (numpy arrays / std::vector, what
+        # a caller of the reference API passes): staged through pinned memory
+        hp_np, hc_np, hh_np = hp.numpy().copy(), np.empty_like(hc.numpy()), np.empty_like(hh.numpy())
+
+        def e2e_pageable():
+            fn = aldp.lib.aldp_lbp_batch_host if k == 0 else aldp.lib.aldp_ldp_batch_host
+            kk = () if k == 0 else (k,)
+            aldp._check(fn(hp_np.ctypes.data, e2n, rows, cols, *kk, cr, cc, hc_np.ctypes.data, hh_np.ctypes.data,
+                           None))
+
+        e2e_pageable()
+        if use_dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_pageable()
+        pg_dt = (time.perf_counter() - t0) / args.steps
+        if use_dist:
+            t = torch.tensor([pg_dt], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            pg_dt = float(t[0])
+        line["e2e"]["pageable_value"] = round(world * e2n * rows * cols / pg_dt / 1e6, 1)
+        line["e2e"]["pageable_note"] = "same call from pageable (non-pinned) host buffers"
         ok = np.array_equal(hc.numpy(), codes[:e2n, :, :cols].cpu().numpy()) and \
-            np.array_equal(hh.numpy(), hist[:e2n].cpu().numpy())
+            np.array_equal(hh.numpy(), (hist[:e2n].to(torch.int64) & 0xFFFF).cpu().numpy()) and \
+            np.array_equal(hc_np, hc.numpy()) and np.array_equal(hh_np, hh.numpy())
         if use_dist:
             t = torch.tensor([0 if ok else 1], device=dev, dtype=torch.int32)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -121,9 +121,11 @@ int aldp_last_launch_count(void);
 
 /* Negative control for parity harnesses (the analogue of the reference's
  * FaultInjection, include/aldp/verify.hpp:14-20): while mode is 1, every
- * batch launch flips bit 0 of image 0's code at (0, 0) and adds one count to
- * bin 0 of image 0's first histogram. 0 turns it off. The environment
- * variable ALDP_FAULT_INJECT sets the initial mode. Returns the old mode. */
+ * aldp_ldp_batch* / aldp_lbp_batch* call ends with a one-thread launch that
+ * flips bit 0 of image 0's code at (0, 0) and adds one count to bin 0 of
+ * image 0's first histogram (the product kernels are untouched). 0 turns it
+ * off. The environment variable ALDP_FAULT_INJECT sets the initial mode.
+ * Returns the old mode. */
 int aldp_debug_fault(int mode);
 
 /* Number of histogram bins for k: C(8, k) (56 for k == 3), 0 if k invalid. */
@@ -172,6 +174,11 @@ aldp_status aldp_lbp_batch_host(const uint8_t* pixels, int n_images, int rows, i
 aldp_status aldp_ldp_batch_host(const uint8_t* pixels, int n_images, int rows, int cols, int k,
                                 int cell_rows, int cell_cols, uint8_t* codes, uint32_t* hist,
                                 void* stream);
+
+/* aldp::make_random (include/aldp/image.hpp:44, reference image.cpp:75-83):
+ * rows x cols bytes, std::mt19937(seed) low byte per pixel, row-major (the
+ * config-1 input). Host memory; rows, cols >= 3. */
+aldp_status aldp_make_random(uint8_t* out, int rows, int cols, uint32_t seed);
 
 /* ---- several GPUs in one process ----
  * aldp_ldp_batch_host over n_devices GPUs: the images are split into

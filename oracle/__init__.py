@@ -360,19 +360,21 @@ def ref_bench_csv(series="images", size=0, counts=(1, 2, 4, 6, 8, 10), windows=(
 
 
 def ref_median_seconds_batch(pixels, k: int = 3, cell=(0, 0), path: int = 1, threads: int = 1,
-                             repeats: int = 3) -> float:
+                             repeats: int = 3, codes: bool = True) -> float:
     """The reference's own timer (bench.cpp:51-78: warm-up pass, batches up to
-    >= 5 ms, median of `repeats`) around ref_batch (codes + histograms)."""
+    >= 5 ms, median of `repeats`) around ref_batch (codes + histograms, or the
+    histograms alone with codes=False: the reference API's one pass)."""
     px = np.ascontiguousarray(pixels, dtype=np.uint8)
     if px.ndim == 2:
         px = px[None]
     n, r, c = px.shape
     nb = ref_n_bins(k)
     cells = 1 if cell[0] == 0 else (r // cell[0]) * (c // cell[1])
-    codes = np.empty_like(px)
+    cbuf = np.empty_like(px) if codes else None
     hist = np.empty((n, cells, nb), np.uint64)
     return float(ref().ref_median_seconds_batch(px.ctypes.data, n, r, c, k, cell[0], cell[1], path,
-                                                 codes.ctypes.data, hist.ctypes.data, threads, repeats))
+                                                 cbuf.ctypes.data if cbuf is not None else None,
+                                                 hist.ctypes.data, threads, repeats))
 
 
 def ref_n_bins(k: int) -> int:

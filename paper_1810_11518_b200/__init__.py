@@ -38,7 +38,7 @@ __all__ = [
     "lbp_histogram", "lbp_code_map", "lbp_batch", "response_field", "response_field_batch",
     "FaultInjection", "Mismatch", "VerifyResult", "verify_equivalence", "verify_image", "verify_batch",
     "PgmError", "load_pgm", "save_pgm", "load_pgm_batch", "extract_files", "op_counts", "bench_csv",
-    "CLI_PATH", "last_launch_count", "debug_fault", "ldp_batch_host_multi",
+    "CLI_PATH", "last_launch_count", "debug_fault", "ldp_batch_host_multi", "make_random",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -129,6 +129,7 @@ def _load() -> ctypes.CDLL:
         "aldp_lbp_code_map": ([P, I, I, P], I),
         "aldp_lbp_batch_host": ([P, I, I, I, I, I, P, P, P], I),
         "aldp_ldp_batch_host_multi": ([P, I, I, I, I, I, I, P, P, P, I], I),
+        "aldp_make_random": ([P, I, I, ctypes.c_uint32], I),
         "aldp_lbp_batch_host_multi": ([P, I, I, I, I, I, P, P, P, I], I),
         "aldp_ldp_batch_multi": ([ctypes.POINTER(_Args), P, P, I], I),
         "aldp_gather_peer": ([P, I, P, P, P, I, P], I),
@@ -155,6 +156,8 @@ def _load() -> ctypes.CDLL:
                             ctypes.c_char_p], I),
     }
     for name, (argtypes, restype) in sig.items():
+        if os.environ.get("ALDP_LIB") and not hasattr(L, name):
+            continue  # an older build under A/B (ALDP_LIB) may predate this entry point
         fn = getattr(L, name)
         fn.argtypes = argtypes
         fn.restype = restype
@@ -406,8 +409,19 @@ def ldp_batch(pixels, rows: int, cols: int, k: int = 3, cell: Tuple[int, int] = 
     return codes, hist
 
 
+def make_random(rows: int, cols: int, seed: int) -> np.ndarray:
+    """aldp::make_random (image.hpp:44; reference image.cpp:75-83): the
+    std::mt19937 low-byte image of config 1, on the host."""
+    out = np.empty((rows, cols), np.uint8)
+    _check(lib.aldp_make_random(out.ctypes.data, int(rows), int(cols), int(seed) & 0xFFFFFFFF))
+    return out
+
+
 def last_launch_count() -> int:
-    """Kernels the last ldp_batch / lbp_batch call on this thread launched."""
+    """Kernels the last ldp_batch / lbp_batch call on this thread launched
+    (-1: a library build without the counter, A/B runs only)."""
+    if not hasattr(lib, "aldp_last_launch_count"):
+        return -1
     return int(lib.aldp_last_launch_count())
 
 

@@ -17,6 +17,7 @@
 // Per-pixel helpers (responses, column terms, ldp_code, bins, generators)
 // are API surface evaluated on the host, written from the reference's
 // documented semantics.
+#include <cstring>
 #include <algorithm>
 #include <bit>
 #include <cctype>
@@ -384,3 +385,10 @@ VerifyResult verify_image(const GrayImage& img, std::optional<FaultInjection> fa
 }
 
 }  // namespace aldp
+
+extern "C" aldp_status aldp_make_random(uint8_t* out, int rows, int cols, uint32_t seed) {
+    if (!out || rows < 3 || cols < 3) return ALDP_EINVAL;
+    const aldp::GrayImage img = aldp::make_random(rows, cols, seed);
+    std::memcpy(out, img.pixels().data(), img.pixels().size());
+    return ALDP_OK;
+}

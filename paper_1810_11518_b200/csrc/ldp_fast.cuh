@@ -78,8 +78,7 @@ struct FastParams {
     int codes_pitch;
     uint32_t* hist;
     int nbins;
-    int hist16;  // hist holds uint16 counts (two bins per 32-bit word)
-    int fault;   // aldp_debug_fault: corrupt image 0's first code and bin
+    int hist16;  // 1: hist holds uint16 counts (two bins per 32-bit word)
     int cell_rows, cell_cols, grid_r, grid_c;  // cell mode only
     int cell_clamp;                            // cell mode: 1 = per-cell clamp, 0 = cut from the code map
     int edge_lo, edge_hi;                      // band rows recounted with the cell clamp (-1: none)
@@ -102,8 +101,7 @@ __host__ __device__ constexpr int fast_tag_set(bool cells) { return cells ? 0 : 
 // hist[idx] += v on uint32 counts, or on uint16 counts packed two per word
 // (a count never reaches 65536 there, so the add cannot carry across bins)
 __device__ __forceinline__ void hist_add(uint32_t* hist, int hist16, int64_t idx, uint32_t v) {
-    if (hist16) atomicAdd(hist + (idx >> 1), v << (16 * int(idx & 1)));
-    else atomicAdd(hist + idx, v);
+    atomicAdd(hist + (idx >> hist16), v << ((uint32_t(idx) & uint32_t(hist16)) << 4));  // branch-free
 }
 
 __device__ __forceinline__ uint32_t fdiv(uint32_t n, uint64_t m, int sh) {
@@ -771,10 +769,6 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
             // the trash region collects masked counts: clear it too
             uint32_t* tr = reinterpret_cast<uint32_t*>(seg_ptr + kMaxTileCells * REGION + CNT);
             for (int j = sl; j < NT; j += SEG) tr[j] = 0;
-        }
-        if (p.fault && seg_live && img == 0 && r0 == 0 && blk == 0 && sl == 0) {  // negative control
-            if (CODES) p.codes[0] ^= 1;
-            if (HIST && do_hist) hist_add(p.hist, p.hist16, 0, 1u);
         }
         __syncwarp();
     }

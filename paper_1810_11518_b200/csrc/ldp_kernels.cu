@@ -83,7 +83,6 @@ struct GenericParams {
     uint32_t* hist;
     int nbins;
     int hist16;                                // uint16 counts, two per word
-    int fault;                                 // aldp_debug_fault
     int cell_rows, cell_cols, grid_r, grid_c;  // cell_rows == 0: whole image
     int cell_clamp;                            // 0: cells cut from the whole-image code map
     int row_lo, row_hi;                        // neighbour rows readable (halo rows of a band view)
@@ -101,11 +100,9 @@ __global__ void ldp_generic_kernel(GenericParams p) {
         // k == 0: LBP (256 bins indexed by the code itself)
         const unsigned code = p.k ? clamped_code(base, p.pitch, x, y, p.row_lo, p.row_hi, 0, p.cols - 1, p.k)
                                   : clamped_lbp(base, p.pitch, x, y, p.row_lo, p.row_hi, 0, p.cols - 1);
-        const bool fault = p.fault && t == 0;  // negative control: image 0, pixel (0, 0)
         if (p.codes)
-            p.codes[img * p.codes_img_stride + int64_t(x) * p.codes_pitch + y] = uint8_t(code ^ (fault ? 1u : 0u));
+            p.codes[img * p.codes_img_stride + int64_t(x) * p.codes_pitch + y] = uint8_t(code);
         if (!p.hist) continue;
-        if (fault) hist_add(p.hist, p.hist16, 0, 1u);
         if (p.cell_rows == 0) {
             hist_add(p.hist, p.hist16, int64_t(img) * p.nbins + (p.k ? colex_rank(code) : code), 1u);
         } else {
@@ -124,6 +121,14 @@ __global__ void ldp_generic_kernel(GenericParams p) {
     }
 }
 
+
+// Negative control (aldp_debug_fault): after a batch, corrupt image 0's code
+// at (0, 0) and its first histogram's bin 0 -- a separate launch, so the
+// product kernels carry no trace of it.
+__global__ void fault_kernel(uint8_t* codes, uint32_t* hist, int hist16) {
+    if (codes) codes[0] ^= 1;
+    if (hist) hist_add(hist, hist16, 0, 1u);
+}
 
 // --------------------------------------------------------------------------
 // dispatch
@@ -285,7 +290,6 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
         if (area >= 65536) return fail(ALDP_EINVAL, "hist_u16: a histogram can reach 65536 counts");
         if (reinterpret_cast<uintptr_t>(a->d_hist) % 4) return fail(ALDP_EINVAL, "hist_u16: d_hist not 4-byte aligned");
     }
-    const int fault = g_fault.load(std::memory_order_relaxed);
     if (a->d_hist)
         ALDP_CUDA_TRY(cudaMemsetAsync(a->d_hist, 0,
                                       (a->hist_u16 ? 2 : 4) * size_t(a->n_images) * cells * nbins, st));
@@ -317,7 +321,6 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
         p.hist = a->d_hist;
         p.nbins = nbins;
         p.hist16 = a->hist_u16 ? 1 : 0;
-        p.fault = fault;
         p.cell_rows = a->cell_rows;
         p.cell_cols = a->cell_cols;
         p.cell_clamp = a->cell_from_map ? 0 : 1;
@@ -338,11 +341,17 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
         // uses the cell clamp anyway) and its code is rewritten by the second
         // launch, which starts two rows above the grid's end with a real row
         // above it. cell_from_map counts map codes, so it keeps one launch.
-        // Only for small batches (under kSplitTiles tiles per warp segment):
-        // the remainder launch recomputes ~1 % of the pixels, more than the
-        // imbalance costs a large batch (C5: -0.5 % split, C2: +4.7 %).
+        // Round 1 split only small batches (C2 +4.7 %, full C5 -0.5 %); with
+        // the round-2 row loop the split pays at every size (full C5: 762 k
+        // -> 794 k Mpixel/s, profiles/r02_split_ab.txt): the remainder launch
+        // recomputes ~1 % of the pixels, but the grid launch then runs tiles
+        // of one height and one code path. ALDP_SPLIT_TILES (tiles per warp
+        // segment below which to split) overrides it for A/B runs.
         // (validate() guarantees grid_r >= 1 here: cell_rows <= rows.)
-        constexpr int64_t kSplitTiles = 64;
+        static const int64_t kSplitTiles = [] {
+            const char* e = std::getenv("ALDP_SPLIT_TILES");
+            return e ? int64_t(std::atoll(e)) : int64_t(1) << 40;
+        }();
         const int grid_rows = grid_r * a->cell_rows;
         const int64_t tiles = int64_t(a->n_images) * ((a->rows + a->cell_rows - 1) / std::max(a->cell_rows, 1)) *
                               ((a->cols + kTileCols - 1) / kTileCols);
@@ -361,7 +370,6 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
             q.rows = a->rows - start;
             q.codes = a->d_codes + int64_t(start) * a->codes_pitch;
             q.hist = nullptr;
-            q.fault = 0;
             q.cell_rows = q.cell_cols = 0;
             q.grid_r = q.grid_c = 1;
             q.edge_lo = q.edge_hi = -1;
@@ -386,7 +394,6 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
     g.hist = a->d_hist;
     g.nbins = nbins;
     g.hist16 = a->hist_u16 ? 1 : 0;
-    g.fault = fault;
     g.cell_rows = a->cell_rows;
     g.cell_cols = a->cell_cols;
     g.cell_clamp = a->cell_from_map ? 0 : 1;
@@ -403,6 +410,17 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
     return ALDP_OK;
 }
 
+// run_batch, then the negative control's corruption when it is on.
+static aldp_status run_batch_checked(const aldp_ldp_args* a, int kernel, cudaStream_t st, bool lbp) {
+    aldp_status s = run_batch(a, kernel, st, lbp);
+    if (s == ALDP_OK && g_fault.load(std::memory_order_relaxed) && a->n_images > 0 && (a->d_codes || a->d_hist)) {
+        fault_kernel<<<1, 1, 0, st>>>(a->d_codes, a->d_hist, a->hist_u16 ? 1 : 0);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "fault_kernel launch");
+    }
+    return s;
+}
+
 }  // namespace aldp_b200
 
 using namespace aldp_b200;
@@ -410,23 +428,23 @@ using namespace aldp_b200;
 extern "C" {
 
 aldp_status aldp_ldp_batch(const aldp_ldp_args* args, void* stream) {
-    return run_batch(args, ALDP_KERNEL_AUTO, static_cast<cudaStream_t>(stream), false);
+    return run_batch_checked(args, ALDP_KERNEL_AUTO, static_cast<cudaStream_t>(stream), false);
 }
 
 aldp_status aldp_ldp_batch_ex(const aldp_ldp_args* args, int kernel, void* stream) {
     if (kernel < ALDP_KERNEL_AUTO || kernel > ALDP_KERNEL_GENERIC)
         return fail(ALDP_EINVAL, "unknown kernel selector");
-    return run_batch(args, kernel, static_cast<cudaStream_t>(stream), false);
+    return run_batch_checked(args, kernel, static_cast<cudaStream_t>(stream), false);
 }
 
 aldp_status aldp_lbp_batch(const aldp_ldp_args* args, void* stream) {
-    return run_batch(args, ALDP_KERNEL_AUTO, static_cast<cudaStream_t>(stream), true);
+    return run_batch_checked(args, ALDP_KERNEL_AUTO, static_cast<cudaStream_t>(stream), true);
 }
 
 aldp_status aldp_lbp_batch_ex(const aldp_ldp_args* args, int kernel, void* stream) {
     if (kernel < ALDP_KERNEL_AUTO || kernel > ALDP_KERNEL_GENERIC)
         return fail(ALDP_EINVAL, "unknown kernel selector");
-    return run_batch(args, kernel, static_cast<cudaStream_t>(stream), true);
+    return run_batch_checked(args, kernel, static_cast<cudaStream_t>(stream), true);
 }
 
 int aldp_n_bins(int k) {

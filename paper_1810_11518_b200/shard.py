@@ -25,31 +25,50 @@ def wire_dtype_ok(max_count: int) -> bool:
     return 0 <= max_count < 65536
 
 
-def gather_histograms(hist, dist, rank: int, world: int, wire=None, out: Optional[List] = None):
-    """Gather every rank's [images, cells, bins] int32 histogram shard to rank 0.
+def gather_histograms(hist, dist, rank: int, world: int, wire=None, out: Optional[List] = None,
+                      max_count: Optional[int] = None):
+    """Gather every rank's [images, cells, bins] histogram shard to rank 0.
 
-    hist : this rank's counts (torch int32; CUDA with NCCL, CPU with gloo)
-    wire : optional preallocated int16 tensor of hist's shape (reused per step)
-    out  : on rank 0, optional list of `world` int16 receive tensors
-    Returns, on rank 0, the list of per-rank int16 shards (rank order =
-    image order); None elsewhere. Shards must be equally sized (NCCL gather).
+    hist : this rank's counts (torch; CUDA with NCCL, CPU with gloo): int16 /
+           uint16 as the kernel writes them for the wire (ldp_batch with an
+           int16 hist), or int32 counts
+    wire : optional preallocated int16 tensor of hist's shape (int32 hist only)
+    out  : on rank 0, optional list of `world` receive tensors (wire dtype)
+    max_count : the largest count a histogram can hold (cell area); int32
+           counts go out as int16 only when it is below 65536 -- checked,
+           not assumed. None: the shard's own maximum decides (one sync).
+    Returns, on rank 0, the list of per-rank shards (rank order = image
+    order; uint16 bit patterns in int16, widen() restores the counts, or
+    int32 when the counts do not fit); None elsewhere. Shards must be equally
+    sized (NCCL gather).
     """
     import torch
-    if wire is None:
-        wire = torch.empty(hist.shape, dtype=torch.int16, device=hist.device)
-    wire.copy_(hist)  # exact: counts < 65536 (wire_dtype_ok), int16 bit pattern
+    if hist.dtype in (torch.int16, torch.uint16):
+        send = hist
+    else:
+        fits = wire_dtype_ok(max_count) if max_count is not None else wire_dtype_ok(int(hist.max()) if
+                                                                                   hist.numel() else 0)
+        if fits:
+            if wire is None:
+                wire = torch.empty(hist.shape, dtype=torch.int16, device=hist.device)
+            wire.copy_(hist)  # exact: counts < 65536, int16 bit pattern
+            send = wire
+        else:
+            send = hist  # counts that can reach 65536 stay int32 on the wire
     if world == 1 and not (dist.is_available() and dist.is_initialized()):
-        return [wire] if rank == 0 else None
+        return [send] if rank == 0 else None
     if rank == 0 and out is None:
-        out = [torch.empty_like(wire) for _ in range(world)]
+        out = [torch.empty_like(send) for _ in range(world)]
     # moved as raw bytes: every backend (NCCL, gloo) carries uint8
-    flat = wire.reshape(-1).view(torch.uint8)
+    flat = send.reshape(-1).view(torch.uint8)
     recv = [o.reshape(-1).view(torch.uint8) for o in out] if rank == 0 else None
     dist.gather(flat, recv, dst=0)
     return out if rank == 0 else None
 
 
 def widen(shards) -> "object":
-    """Rank-0 helper: concatenate int16 shards back to exact int64 counts."""
+    """Rank-0 helper: concatenate gathered shards back to exact int64 counts
+    (int16 shards carry uint16 bit patterns)."""
     import torch
-    return torch.cat([s.to(torch.int64) & 0xFFFF for s in shards], dim=0)
+    return torch.cat([s.to(torch.int64) & 0xFFFF if s.dtype in (torch.int16, torch.uint16) else s.to(torch.int64)
+                      for s in shards], dim=0)

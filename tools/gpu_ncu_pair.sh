@@ -10,7 +10,7 @@ i=0
 for lib in "$@"; do
   i=$((i+1))
   env ALDP_LIB=$lib $CMD > gpurun_out/${TAG}_plain_$i.json 2> gpurun_out/${TAG}_plain_$i.err && \
-  ncu --set full --import-source on --clock-control none -k regex:ldp_fast_kernel -s 3 -c 1 \
+  ncu --set full --import-source on --clock-control none --kernel-name-base mangled -k regex:${KREGEX:-ldp_fast_kernelILi3ELi2ELb1ELb1ELb1} -s 3 -c 1 \
       -o gpurun_out/${TAG}_$i env ALDP_LIB=$lib $CMD > gpurun_out/${TAG}_ncu_$i.log 2>&1
   echo "$i $lib rc=$?" >> gpurun_out/${TAG}_index.txt
 done
