@@ -56,6 +56,10 @@ CONFIGS = {
     "c5w": (65536, 490, 640, 3, 0, 0, 20, "faces", 11518),
     # LBP (k = 0 selects the LBP descriptor) on the C5 batch
     "c5lbp": (65536, 490, 640, 0, 81, 91, 20, "faces", 11518),
+    # the paper's window series (Table 3, windowed_features with
+    # square windows of 10 / 25 px) on 2048 C5 frames: the narrow-cell kernel
+    "w10": (2048, 490, 640, 3, 10, 10, 20, "faces", 11518),
+    "w25": (2048, 490, 640, 3, 25, 25, 20, "faces", 11518),
 }
 WORKLOAD_NAMES = {
     "c5": "C5: 65536 x 640x490 face-like, LDP k=3, code map + 7x6 cell histograms",
@@ -65,6 +69,8 @@ WORKLOAD_NAMES = {
     "c1": "C1: 640x490 uniform random (make_random), LDP k=3, code map + histogram",
     "c5w": "C5 images, whole-image histograms (diagnostic)",
     "c5lbp": "C5 images, LBP (256-bin) code map + 7x6 cell histograms",
+    "w10": "2048 C5 frames, LDP k=3, code map + windowed_features(window=10): 49x64 cells of 10x10",
+    "w25": "2048 C5 frames, LDP k=3, code map + windowed_features(window=25): 19x25 cells of 25x25",
 }
 
 
@@ -224,7 +230,7 @@ def run_reference(args, cfg_name):
     if args.k >= 0:
         k = args.k
     threads = os.cpu_count() or 1
-    sample = max(threads * 4, 32) if cfg_name in ("c5", "c2", "c5w", "c5lbp") else \
+    sample = max(threads * 4, 32) if cfg_name in ("c5", "c2", "c5w", "c5lbp", "w10", "w25") else \
         (threads if cfg_name == "c3" else 1)
     # Inputs: the product arm's own bytes -- the device generator's output for
     # images 0 .. sample-1 (or C4's first 1024 rows), copied back before any

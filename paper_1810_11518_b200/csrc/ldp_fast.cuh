@@ -42,26 +42,31 @@ constexpr int kFastWarps = 8;
 constexpr int kTileCols = 128;
 constexpr int kMaxTileCells = 5;
 constexpr uint32_t kScaleMask = 0x3FC03FC0u;  // bytes 0 and 2 of a word, scaled by 64
-// Per-segment shared layout: kMaxTileCells regions + 1 trash region
-// (FastLayout below).
-constexpr int kSegRegions = kMaxTileCells + 1;
-constexpr int kFixList = 16;                      // border columns per segment (max)
+constexpr int kNarrowTileCells = 16;  // narrow cells (>= 9 columns): up to 16 per 128-column tile
+constexpr int kFixList = 16;          // border columns per segment (max), regular tiles
 // Shared-memory layout of one fast-kernel CTA (the launcher sizes the
-// dynamic allocation from it): per (warp, segment) kSegRegions regions, one
-// per cell a tile can touch plus a trash region. LDP region: a copy of the
-// id -> code table, then the counts (CNT bytes in), so one slot address
-// serves the code lookup (LDS [a - CNT]) and the count (RED [a]). LBP: 256
-// counts. Each region's table and counts are stored XOR-permuted by a bank
-// skew (slot_skew) so that lanes of different segments or cells that hold
-// the same id hit different banks.
-template <int K, int NW>
+// dynamic allocation from it): per (warp, segment) NC + 1 regions, one per
+// cell a tile can touch plus a trash region. Regular tiles (NC =
+// kMaxTileCells): an LDP region holds a copy of the id -> code table, then
+// the counts (CNT bytes in), so one slot address serves the code lookup
+// (LDS [a - CNT]) and the count (RED [a]); LBP: 256 counts. Narrow tiles (NC
+// = kNarrowTileCells, LDP k != 4 only): count-only regions and one code table
+// per segment after them (one more LOP3 per pixel for its address). Each
+// region's table and counts are stored XOR-permuted by a bank skew
+// (slot_skew) so that lanes of different segments or cells that hold the
+// same id hit different banks.
+template <int K, int NW, int NC = kMaxTileCells>
 struct FastLayout {
+    static constexpr bool NARROW = NC > kMaxTileCells;
+    static_assert(!NARROW || (K != 0 && K != 4), "narrow tiles: LDP with 64 ids only");
     static constexpr int NT = K == 0 ? 256 : (K == 4 ? 128 : 64);  // table entries (codes / ids)
-    static constexpr int CNT = K == 0 ? 0 : NT * 4;                 // offset of the counts in a region
-    static constexpr int REGION = K == 0 ? 1024 : 2 * NT * 4;
+    static constexpr int CNT = (K == 0 || NARROW) ? 0 : NT * 4;     // offset of the counts in a region
+    static constexpr int REGION = K == 0 ? 1024 : (NARROW ? NT * 4 : 2 * NT * 4);
     static constexpr int NSEG = 32 / (kTileCols / (4 * NW));
-    static constexpr int SEG_SMEM = kSegRegions * REGION;
+    static constexpr int REGIONS = NC + 1 + (NARROW ? 1 : 0);  // cells, trash (, code table)
+    static constexpr int SEG_SMEM = REGIONS * REGION;
     static constexpr int BYTES = kFastWarps * NSEG * SEG_SMEM + REGION;  // + alignment slack
+    static constexpr int FIX = NARROW ? 2 * NC + 2 : kFixList;          // border columns per segment
 };
 
 // Bank skew (word XOR, < 32) of segment `seg`'s region `lc`.
@@ -263,11 +268,12 @@ __device__ __forceinline__ void load_words(const uint8_t* p, uint32_t (&w)[NW]) 
 // HALO: the view is a band of a taller resident frame (rows -1 / rows are
 // real neighbours); a separate instantiation keeps the common path's row
 // clamp a compile-time [0, rows) (a runtime bound measured 1.8 % slower).
-template <int K, int NW, bool CELLS, bool CODES, bool HIST, bool HALO = false>
+template <int K, int NW, bool CELLS, bool CODES, bool HIST, bool HALO = false, int NC = kMaxTileCells>
 __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_kernel(FastParams p) {
     constexpr bool LBP = K == 0;
     constexpr int TS = fast_tag_set(CELLS);  // the host builds the id tables for the same set
-    using Lay = FastLayout<K, NW>;
+    using Lay = FastLayout<K, NW, NC>;
+    constexpr bool NARROW = Lay::NARROW;
     constexpr int REGION = Lay::REGION, CNT = Lay::CNT, NT = Lay::NT, SEG_SMEM = Lay::SEG_SMEM;
     constexpr int LC = 4 * NW;              // columns per lane
     constexpr int SEG = kTileCols / LC;     // lanes per segment (tile)
@@ -280,7 +286,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
     constexpr int SUMS = CELLS ? ALDP_CELL_SUMS : 2;  // measured: all stored sums win only without cells
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint8_t id_bin[128];
-    __shared__ int fix_cols[kFastWarps][NSEG][kFixList];
+    __shared__ int fix_cols[kFastWarps][NSEG][Lay::FIX];
     __shared__ int fix_n[kFastWarps][NSEG];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -300,8 +306,9 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
         const int words = kFastWarps * NSEG * SEG_SMEM / 4;
         for (int i = threadIdx.x; i < words; i += blockDim.x) {
             const int in_region = i & (REGION / 4 - 1);
-            const int region = (i / (REGION / 4)) % kSegRegions, sg = (i / (SEG_SMEM / 4)) % NSEG;
-            w[i] = (!LBP && in_region < NT) ? uint32_t(p.id_code[in_region ^ slot_skew(sg, region)]) : 0u;
+            const int region = (i / (REGION / 4)) % Lay::REGIONS, sg = (i / (SEG_SMEM / 4)) % NSEG;
+            const bool table = !LBP && (NARROW ? region == NC + 1 : in_region < NT);
+            w[i] = table ? uint32_t(p.id_code[NARROW ? in_region : in_region ^ slot_skew(sg, region)]) : 0u;
         }
         if (!LBP && threadIdx.x < NT) id_bin[threadIdx.x] = p.id_bin[threadIdx.x];
     }
@@ -344,7 +351,8 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
     const uint32_t src_prev = seg_lane0 + uint32_t((sl + SEG - 1) % SEG);
     const uint32_t src_next = seg_lane0 + uint32_t((sl + 1) % SEG);
     // masked pixels count here; codes-only launches look codes up here too
-    const uint32_t trash = seg_base + kMaxTileCells * REGION + CNT + slot_skew(seg, kMaxTileCells) * 4;
+    const uint32_t trash = seg_base + NC * REGION + CNT + slot_skew(seg, NC) * 4;
+    const uint32_t code_tab = seg_base + (NC + 1) * REGION;  // narrow tiles: the segment's id -> code table
     const uint32_t one = p.one;
     // Band b of an image -> first row, height, cell row (cell mode: bands
     // are cell rows, then the rows below the grid, crow == grid_r).
@@ -522,6 +530,16 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
                 ad[s_hi] = (LBP ? (X[q] >> 6) & M : __umulhi(X[q], 1u << 18) & M) ^ slot[s_hi];
             }
         };
+        // narrow tiles: code-table addresses of the same ids
+        auto code_addrs = [&](const uint32_t (&X)[NPAIR], uint32_t (&cd)[LC]) {
+#pragma unroll
+            for (int q = 0; q < NPAIR; ++q) {
+                const int s_lo = (q >> 1) * 4 + (q & 1), s_hi = s_lo + 2;
+                constexpr uint32_t M = (NT - 1) * 4;
+                cd[s_lo] = ((X[q] * 4u) & M) | code_tab;
+                cd[s_hi] = (__umulhi(X[q], 1u << 18) & M) | code_tab;
+            }
+        };
         // count the lane's pixels at slot addresses ad
         auto count = [&](const uint32_t (&ad)[LC]) {
 #pragma unroll
@@ -567,8 +585,15 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
                         wd[j] = prmt(X[2 * j], X[2 * j + 1], 0x5140);
                 } else {
                     uint32_t e[LC];
+                    if constexpr (NARROW) {
+                        uint32_t cd[LC];
+                        code_addrs(X, cd);
 #pragma unroll
-                    for (int s = 0; s < LC; ++s) e[s] = lds32(ad[s] - CNT);
+                        for (int s = 0; s < LC; ++s) e[s] = lds32(cd[s]);
+                    } else {
+#pragma unroll
+                        for (int s = 0; s < LC; ++s) e[s] = lds32(ad[s] - CNT);
+                    }
 #pragma unroll
                     for (int j = 0; j < NW; ++j)  // bytes -> word with multiply-adds (FMA pipe)
                         wd[j] = e[4 * j] + e[4 * j + 1] * 0x100u + e[4 * j + 2] * 0x10000u + e[4 * j + 3] * 0x1000000u;
@@ -658,8 +683,8 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
                     const int c_end = min(c0 + kTileCols, p.grid_c * p.cell_cols);
                     for (int cc = cell_c0; cc * p.cell_cols < c_end; ++cc) {
                         const int left = cc * p.cell_cols, right = left + p.cell_cols - 1;
-                        if (left >= c0 && left > 0 && n < kFixList) fl[n++] = left;
-                        if (right >= c0 && right < c_end && right < last && n < kFixList) fl[n++] = right;
+                        if (left >= c0 && left > 0 && n < Lay::FIX) fl[n++] = left;
+                        if (right >= c0 && right < c_end && right < last && n < Lay::FIX) fl[n++] = right;
                     }
                 }
                 fix_n[warp][seg] = n;
@@ -767,7 +792,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
                 }
             }
             // the trash region collects masked counts: clear it too
-            uint32_t* tr = reinterpret_cast<uint32_t*>(seg_ptr + kMaxTileCells * REGION + CNT);
+            uint32_t* tr = reinterpret_cast<uint32_t*>(seg_ptr + NC * REGION + CNT);
             for (int j = sl; j < NT; j += SEG) tr[j] = 0;
         }
         __syncwarp();

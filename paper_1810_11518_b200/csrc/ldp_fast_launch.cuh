@@ -24,11 +24,11 @@ inline aldp_status fast_cuda_fail(cudaError_t e, const char* what) {
     return set_error(ALDP_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-template <int K, int NW, bool CELLS, bool CODES, bool HIST, bool HALO>
+template <int K, int NW, bool CELLS, bool CODES, bool HIST, bool HALO, int NC = kMaxTileCells>
 aldp_status launch_fast_t(const FastParams& p, cudaStream_t st) {
-    auto kern = ldp_fast_kernel<K, NW, CELLS, CODES, HIST, HALO>;
-    constexpr int NSEG = FastLayout<K, NW>::NSEG;
-    const size_t smem = FastLayout<K, NW>::BYTES;
+    auto kern = ldp_fast_kernel<K, NW, CELLS, CODES, HIST, HALO, NC>;
+    constexpr int NSEG = FastLayout<K, NW, NC>::NSEG;
+    const size_t smem = FastLayout<K, NW, NC>::BYTES;
     // The shared-memory opt-in is a per-device function attribute: set it once
     // per device this process launches on (several GPUs in one process work).
     constexpr int kMaxDev = 64;
@@ -65,6 +65,15 @@ aldp_status launch_fast_t(const FastParams& p, cudaStream_t st) {
     X aldp_status launch_fast_t<K, 2, true, false, true, false>(const FastParams&, cudaStream_t); \
     X aldp_status launch_fast_t<K, 2, true, true, true, true>(const FastParams&, cudaStream_t);   \
     X aldp_status launch_fast_t<K, 2, true, false, true, true>(const FastParams&, cudaStream_t);
+// Narrow cells (9 .. 31 columns: up to kNarrowTileCells per tile), LDP k != 4.
+#define ALDP_FAST_NARROW_INST_K(X, K)                                                                             \
+    X aldp_status launch_fast_t<K, 2, true, true, true, false, kNarrowTileCells>(const FastParams&, cudaStream_t);  \
+    X aldp_status launch_fast_t<K, 2, true, false, true, false, kNarrowTileCells>(const FastParams&, cudaStream_t); \
+    X aldp_status launch_fast_t<K, 2, true, true, true, true, kNarrowTileCells>(const FastParams&, cudaStream_t);   \
+    X aldp_status launch_fast_t<K, 2, true, false, true, true, kNarrowTileCells>(const FastParams&, cudaStream_t);
+#define ALDP_FAST_NARROW_INSTANTIATIONS(X)                                                    \
+    ALDP_FAST_NARROW_INST_K(X, 1) ALDP_FAST_NARROW_INST_K(X, 2) ALDP_FAST_NARROW_INST_K(X, 3) \
+    ALDP_FAST_NARROW_INST_K(X, 5) ALDP_FAST_NARROW_INST_K(X, 6) ALDP_FAST_NARROW_INST_K(X, 7)
 #define ALDP_FAST_CELL_INSTANTIATIONS(X)                                              \
     ALDP_FAST_CELL_INST_K(X, 0) ALDP_FAST_CELL_INST_K(X, 1) ALDP_FAST_CELL_INST_K(X, 2) \
     ALDP_FAST_CELL_INST_K(X, 3) ALDP_FAST_CELL_INST_K(X, 4) ALDP_FAST_CELL_INST_K(X, 5) \

@@ -151,10 +151,16 @@ static int n_sms() {
 // options), the rest here.
 int fast_n_sms() { return n_sms(); }
 ALDP_FAST_CELL_INSTANTIATIONS(extern template)
+ALDP_FAST_NARROW_INSTANTIATIONS(extern template)
 
 template <int K, int NW, bool HALO>
-static aldp_status launch_fast_kw(const FastParams& p, bool cells, cudaStream_t st) {
+static aldp_status launch_fast_kw(const FastParams& p, bool cells, bool narrow, cudaStream_t st) {
     const bool codes = p.codes != nullptr, hist = p.hist != nullptr;
+    if constexpr (K != 0 && K != 4) {
+        if (cells && narrow)
+            return codes ? launch_fast_t<K, NW, true, true, true, HALO, kNarrowTileCells>(p, st)
+                         : launch_fast_t<K, NW, true, false, true, HALO, kNarrowTileCells>(p, st);
+    }
     if (cells) {  // cell geometry only matters for histograms
         return codes ? launch_fast_t<K, NW, true, true, true, HALO>(p, st)
                      : launch_fast_t<K, NW, true, false, true, HALO>(p, st);
@@ -168,21 +174,21 @@ static aldp_status launch_fast_kw(const FastParams& p, bool cells, cudaStream_t 
 constexpr int kLaneWords = 2;
 
 template <int K>
-static aldp_status launch_fast_k(const FastParams& p, bool cells, bool halo, cudaStream_t st) {
-    return halo ? launch_fast_kw<K, kLaneWords, true>(p, cells, st)
-                : launch_fast_kw<K, kLaneWords, false>(p, cells, st);
+static aldp_status launch_fast_k(const FastParams& p, bool cells, bool narrow, bool halo, cudaStream_t st) {
+    return halo ? launch_fast_kw<K, kLaneWords, true>(p, cells, narrow, st)
+                : launch_fast_kw<K, kLaneWords, false>(p, cells, narrow, st);
 }
 
-static aldp_status launch_fast(const FastParams& p, int k, bool cells, bool halo, cudaStream_t st) {
+static aldp_status launch_fast(const FastParams& p, int k, bool cells, bool narrow, bool halo, cudaStream_t st) {
     switch (k) {
-    case 0: return launch_fast_k<0>(p, cells, halo, st);  // LBP
-    case 1: return launch_fast_k<1>(p, cells, halo, st);
-    case 2: return launch_fast_k<2>(p, cells, halo, st);
-    case 3: return launch_fast_k<3>(p, cells, halo, st);
-    case 4: return launch_fast_k<4>(p, cells, halo, st);
-    case 5: return launch_fast_k<5>(p, cells, halo, st);
-    case 6: return launch_fast_k<6>(p, cells, halo, st);
-    case 7: return launch_fast_k<7>(p, cells, halo, st);
+    case 0: return launch_fast_k<0>(p, cells, narrow, halo, st);  // LBP
+    case 1: return launch_fast_k<1>(p, cells, narrow, halo, st);
+    case 2: return launch_fast_k<2>(p, cells, narrow, halo, st);
+    case 3: return launch_fast_k<3>(p, cells, narrow, halo, st);
+    case 4: return launch_fast_k<4>(p, cells, narrow, halo, st);
+    case 5: return launch_fast_k<5>(p, cells, narrow, halo, st);
+    case 6: return launch_fast_k<6>(p, cells, narrow, halo, st);
+    case 7: return launch_fast_k<7>(p, cells, narrow, halo, st);
     default: return fail(ALDP_EINVAL, "fast kernel: unsupported k");
     }
 }
@@ -241,7 +247,7 @@ static void magic_div(uint32_t d, uint64_t& m, int& sh) {
 // cells: cell histograms (the cell kernel and tag set 0); halo: p is a band
 // view whose edge rows may see real rows (row_lo / row_hi).
 static aldp_status finish_fast(FastParams& p, int n_images, int cell_rows, int cell_cols, int k, bool cells,
-                               bool halo, cudaStream_t st) {
+                               bool halo, cudaStream_t st, bool narrow = false) {
     p.band_rows = cell_rows ? cell_rows : 128;
     if (!cell_rows) {
         // Small batches (a few frames per call): shorter bands until the
@@ -273,7 +279,7 @@ static aldp_status finish_fast(FastParams& p, int n_images, int cell_rows, int c
             p.id_code[id] = uint8_t(c);
             p.id_bin[id] = uint8_t(colex_rank(c));
         }
-    return launch_fast(p, k, cells, halo, st);
+    return launch_fast(p, k, cells, narrow, halo, st);
 }
 
 // lbp: the LBP descriptor (256 bins, k ignored); internally k == 0.
@@ -301,12 +307,15 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
         (reinterpret_cast<uintptr_t>(a->d_pixels) % al) == 0 &&
         (!a->d_codes || (a->codes_pitch % al == 0 && (reinterpret_cast<uintptr_t>(a->d_codes) % al) == 0 &&
                          (a->n_images <= 1 || a->codes_img_stride % al == 0)));
+    // cells per 128-column tile: up to kMaxTileCells on the regular layout,
+    // kNarrowTileCells on the narrow one (LDP k != 4, cells of >= 9 columns)
     int ncl = 1;
-    if (a->cell_rows) ncl = max_cells_per_tile(a->cols, a->cell_cols, grid_c);
-    const bool fast_ok = aligned && ncl <= kMaxTileCells;
+    if (a->cell_rows && a->d_hist) ncl = max_cells_per_tile(a->cols, a->cell_cols, grid_c);
+    const bool narrow = ncl > kMaxTileCells;
+    const bool fast_ok = aligned && (!narrow || (ncl <= kNarrowTileCells && a->cell_cols >= 9 && !lbp && a->k != 4));
     if (kernel == ALDP_KERNEL_FAST && !fast_ok)
-        return fail(ALDP_EINVAL, "fast kernel needs 8-byte aligned pitches/strides "
-                                 "and at most 5 cells per 128 columns");
+        return fail(ALDP_EINVAL, "fast kernel needs 8-byte aligned pitches/strides and at most 5 cells per "
+                                 "128 columns (16 for LDP k != 4 with cells of >= 9 columns)");
     if (kernel != ALDP_KERNEL_GENERIC && fast_ok) {
         FastParams p{};
         p.px = a->d_pixels;
@@ -361,7 +370,7 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
             p.rows = grid_rows;
             p.row_hi = grid_rows - 1;
             if (aldp_status s1 = finish_fast(p, a->n_images, a->cell_rows, a->cell_cols, k, a->d_hist != nullptr,
-                                             a->rows_above != 0, st);
+                                             a->rows_above != 0, st, narrow);
                 s1 != ALDP_OK)
                 return s1;
             if (!a->d_codes) return ALDP_OK;
@@ -378,7 +387,7 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
             return finish_fast(q, a->n_images, 0, 0, k, false, true, st);
         }
         return finish_fast(p, a->n_images, a->cell_rows, a->cell_cols, k, a->cell_rows != 0 && a->d_hist != nullptr,
-                           a->rows_above || a->rows_below, st);
+                           a->rows_above || a->rows_below, st, narrow);
     }
     GenericParams g{};
     g.px = a->d_pixels;

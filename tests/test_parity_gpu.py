@@ -546,3 +546,51 @@ def test_small_batch_split_launch(k, rows, cell):
     # the band's cells are clamped as their own images (windowed_features)
     _, want_band_h = oracle.batch(tall[:1, 1:rows + 1], k=k, cell=cell, codes=False)
     assert np.array_equal(hist.cpu().numpy().astype(np.uint64), want_band_h), (k, rows, cell)
+
+
+# ------------------------------------------------- narrow cells (round 2)
+
+@pytest.mark.parametrize("window", [9, 10, 13, 20, 25, 31])
+@pytest.mark.parametrize("k", [1, 3, 5, 7])
+def test_narrow_cells_fast_kernel(window, k):
+    """The paper's small windows (Table 3: 10, 20, 25 px) on the
+    narrow-cell layout of the packed kernel (up to 16 cells per tile): code
+    maps and every cell's histogram bit-exact vs the oracle, on face-like and
+    tie-heavy frames, frames whose width is not a multiple of 128 included."""
+    faces = aldp.gen_faces(3, 200, 330, blobs=8, seed=window * 7 + k, device=DEV)
+    ties = aldp.gen_ties(2, 150, 256, seed=window + k, device=DEV)
+    for px, r, c in ((faces, 200, 330), (ties, 150, 256)):
+        codes, hist = aldp.ldp_batch(px, r, c, k=k, cell=(window, window), codes=True, hist=True, kernel="fast")
+        assert aldp.last_launch_count() >= 1
+        torch.cuda.synchronize()
+        host = px[:, :, :c].cpu().numpy()
+        rc, rh = oracle.batch(host, k=k, cell=(window, window))
+        assert np.array_equal(codes[:, :, :c].cpu().numpy(), rc), (window, k)
+        assert np.array_equal(hist.cpu().numpy().astype(np.uint64), rh), (window, k)
+
+
+def test_narrow_cells_rectangular_and_paper_windows():
+    """Rectangular narrow cells and the full 640x490 frame at windows 10 / 20 /
+    25 (the reference's windowed_features, 3136 / 768 / 475 cells)."""
+    px = aldp.gen_faces(2, 490, 640, blobs=20, seed=99, device=DEV)
+    host = px[:, :, :640].cpu().numpy()
+    for cell in ((10, 10), (20, 20), (25, 25), (12, 9), (40, 11), (7, 30)):
+        _, hist = aldp.ldp_batch(px, 490, 640, k=3, cell=cell, hist=True)
+        torch.cuda.synchronize()
+        _, rh = oracle.batch(host, k=3, cell=cell, codes=False)
+        assert np.array_equal(hist.cpu().numpy().astype(np.uint64), rh), cell
+
+
+def test_narrow_cells_fallbacks():
+    """Cells narrower than 9 columns, LBP and k = 4 on narrow cells run the
+    generic kernel under kernel='auto' (bit-exact) and are refused by 'fast'."""
+    px = aldp.gen_faces(1, 64, 160, seed=5, device=DEV)
+    host = px[:, :, :160].cpu().numpy()
+    for k, cell in ((3, (8, 8)), (3, (5, 3)), (4, (10, 10)), (0, (10, 10))):
+        c, h = aldp.ldp_batch(px, 64, 160, k=k, cell=cell, codes=True, hist=True)
+        torch.cuda.synchronize()
+        rc, rh = oracle.batch(host, k=k, cell=cell)
+        assert np.array_equal(c[:, :, :160].cpu().numpy(), rc) and \
+            np.array_equal(h.cpu().numpy().astype(np.uint64), rh), (k, cell)
+        with pytest.raises(ValueError):
+            aldp.ldp_batch(px, 64, 160, k=k, cell=cell, codes=True, hist=True, kernel="fast")
