@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
 #endif
     constexpr int SUMS = CELLS ? ALDP_CELL_SUMS : 2;  // measured: all stored sums win only without cells
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ uint8_t id_bin[128];
+    __shared__ __align__(4) uint8_t id_bin[128];
     __shared__ int fix_cols[kFastWarps][NSEG][Lay::FIX];
     __shared__ int fix_n[kFastWarps][NSEG];
 
@@ -676,18 +676,22 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
 
         // ---- cell border columns: recount with the cell clamp ----
         if (HIST && CELLS && p.cell_clamp && __any_sync(FULL, do_hist)) {
+            // The segment's border columns, one cell per lane (a tile touches
+            // at most SEG cells), compacted in cell order with ballots.
             int* fl = fix_cols[warp][seg];
-            if (sl == 0) {
-                int n = 0;
-                if (do_hist) {
-                    const int c_end = min(c0 + kTileCols, p.grid_c * p.cell_cols);
-                    for (int cc = cell_c0; cc * p.cell_cols < c_end; ++cc) {
-                        const int left = cc * p.cell_cols, right = left + p.cell_cols - 1;
-                        if (left >= c0 && left > 0 && n < Lay::FIX) fl[n++] = left;
-                        if (right >= c0 && right < c_end && right < last && n < Lay::FIX) fl[n++] = right;
-                    }
-                }
-                fix_n[warp][seg] = n;
+            {
+                const int c_end = min(c0 + kTileCols, p.grid_c * p.cell_cols);
+                const int left = (cell_c0 + sl) * p.cell_cols, right = left + p.cell_cols - 1;
+                const bool in_tile = do_hist && left < c_end;
+                const bool okl = in_tile && left >= c0 && left > 0;
+                const bool okr = in_tile && right >= c0 && right < c_end && right < last;
+                const unsigned seg_mask = (SEG == 32 ? FULL : ((1u << SEG) - 1u)) << (seg * SEG);
+                const unsigned bl = __ballot_sync(FULL, okl) & seg_mask, br = __ballot_sync(FULL, okr) & seg_mask;
+                const unsigned below = (1u << lane) - 1u;
+                const int pos = __popc(bl & below) + __popc(br & below);
+                if (okl) fl[pos] = left;
+                if (okr) fl[pos + (okl ? 1 : 0)] = right;
+                if (sl == 0) fix_n[warp][seg] = __popc(bl) + __popc(br);
             }
             __syncwarp();
             // Vertical runs: the segment's 2*SEG u16 half-slots split the
@@ -780,20 +784,40 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
             }
             const int64_t cells_per_image = CELLS ? int64_t(p.grid_r) * p.grid_c : 1;
             uint8_t* seg_ptr = smem_al + (seg_base - smem_base);
-            for (int j = sl; j < ntab * NT; j += SEG) {
-                const int lc = j / NT, wi = j % NT, id = wi ^ int(slot_skew(seg, lc));
-                uint32_t* cnt = reinterpret_cast<uint32_t*>(seg_ptr + lc * REGION + CNT);
-                const uint32_t v = cnt[wi];
-                if (v) {
-                    const int64_t cell = CELLS ? int64_t(crow) * p.grid_c + cell_c0 + lc : 0;
-                    const int bin = LBP ? id : id_bin[id];
-                    hist_add(p.hist, p.hist16, (int64_t(img) * cells_per_image + cell) * p.nbins + bin, v);
-                    cnt[wi] = 0;
+            // four counts per 128-bit load: the bank skew is a multiple of 8
+            // words, so words 4g .. 4g+3 hold ids (4g ^ skew) .. + 3
+            constexpr int G4 = NT / 4;
+            for (int g = sl; g < ntab * G4; g += SEG) {
+                const int lc = g / G4, w4 = (g % G4) * 4;
+                uint4* q = reinterpret_cast<uint4*>(seg_ptr + lc * REGION + CNT) + (w4 >> 2);
+                const uint4 v = *q;
+                if (v.x | v.y | v.z | v.w) {
+                    const int id0 = w4 ^ int(slot_skew(seg, lc));
+                    // bins of ids id0 .. id0+3: one word of the byte table
+                    const uint32_t b4 = LBP ? 0u : reinterpret_cast<const uint32_t*>(id_bin)[id0 >> 2];
+                    const int64_t base =
+                        (int64_t(img) * cells_per_image + (CELLS ? int64_t(crow) * p.grid_c + cell_c0 + lc : 0)) *
+                        p.nbins;  // even (every bin count is even)
+                    const uint32_t c4[4] = {v.x, v.y, v.z, v.w};
+                    if (!p.hist16) {
+                        uint32_t* hp = p.hist + base;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            if (c4[j]) atomicAdd(hp + (LBP ? id0 + j : (b4 >> (8 * j)) & 0xFFu), c4[j]);
+                    } else {  // uint16 counts, two bins per word
+                        uint32_t* hp = p.hist + (base >> 1);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const uint32_t bin = LBP ? uint32_t(id0 + j) : (b4 >> (8 * j)) & 0xFFu;
+                            if (c4[j]) atomicAdd(hp + (bin >> 1), c4[j] << ((bin & 1u) << 4));
+                        }
+                    }
+                    *q = make_uint4(0u, 0u, 0u, 0u);
                 }
             }
             // the trash region collects masked counts: clear it too
-            uint32_t* tr = reinterpret_cast<uint32_t*>(seg_ptr + NC * REGION + CNT);
-            for (int j = sl; j < NT; j += SEG) tr[j] = 0;
+            uint4* tr = reinterpret_cast<uint4*>(seg_ptr + NC * REGION + CNT);
+            for (int j = sl; j < G4; j += SEG) tr[j] = make_uint4(0u, 0u, 0u, 0u);
         }
         __syncwarp();
     }
