@@ -69,6 +69,12 @@ struct FastLayout {
     static constexpr int FIX = NARROW ? 2 * NC + 2 : kFixList;          // border columns per segment
 };
 
+#ifndef ALDP_MINB
+#define ALDP_MINB 2  // CTAs per SM the register allocation targets (NW = 2)
+#endif
+#ifndef ALDP_KEYS
+#define ALDP_KEYS 2  // odd keys of tag set 0 formed on the FMA pipe: 0 = none, 2 = K1/K7, 3 = all four (A/B: DESIGN 6)
+#endif
 // Bank skew (word XOR, < 32) of segment `seg`'s region `lc`.
 __host__ __device__ constexpr uint32_t slot_skew(int seg, int lc) { return uint32_t(seg * 16 + lc * 8) & 31u; }
 
@@ -94,9 +100,13 @@ struct FastParams {
     int sh_group, sh_bandG, sh_band1, sh_blocks, sh_cell;
     int band_rows, bands, blocks;
     int64_t n_tiles;
+    // narrow cells: store the cells wholly inside a tile, add the ones that
+    // straddle a tile edge (zeroed beforehand by zero_straddling_cells)
+    int store_whole;
     uint32_t one;         // 1 at run time: multiplier that keeps integer adds on the FMA pipe
     uint8_t id_code[128];  // id -> code (0 where no code has that id); 7-bit ids for k == 4
     uint8_t id_bin[128];   // id -> histogram bin (colex rank of the code)
+    uint8_t bin_id[64];    // histogram bin -> id (narrow cells stored whole)
 };
 
 // Tag set of a fast-kernel instantiation (ldp_common.cuh kTagT): the cell
@@ -127,6 +137,13 @@ __device__ __forceinline__ uint32_t fadd(uint32_t a, uint32_t b, uint32_t one) {
     return r;
 }
 
+// a + IMM on the FMA pipe (IMAD with the unknown-to-the-compiler `one`)
+template <uint32_t IMM>
+__device__ __forceinline__ uint32_t faddc(uint32_t a, uint32_t one) {
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(one), "n"(IMM));
+    return r;
+}
 // Column registers of one pixel pair: left/centre/right and the pair sums
 // lc = l + c, cr = c + r (all scaled by 64).
 struct Col {
@@ -166,9 +183,21 @@ __device__ __forceinline__ uint32_t pair_id(const Col& a, const Col& b, const Co
         // (one pre-add + VIADDMNMX): 16 instructions per pair. Measured and
         // rejected for this kernel: sums on the FMA pipe
         // (IMAD), the tag-set-1 scheme above, FMA-pipe slot addresses.
-        const uint32_t k1 = a.cr + b.r + T1, k3 = a.lc + b.l + T3;
-        const uint32_t k5 = c.lc + b.l + T5, k7 = c.cr + b.r + T7;
+#if ALDP_KEYS >= 2
+        const uint32_t k1 = fadd(faddc<T1>(a.cr, one), b.r, one), k7 = fadd(faddc<T7>(c.cr, one), b.r, one);
+#else
+        const uint32_t k1 = a.cr + b.r + T1, k7 = c.cr + b.r + T7;
+#endif
+#if ALDP_KEYS >= 3
+        const uint32_t k3 = fadd(faddc<T3>(a.lc, one), b.l, one), k5 = fadd(faddc<T5>(c.lc, one), b.l, one);
+#else
+        const uint32_t k3 = a.lc + b.l + T3, k5 = c.lc + b.l + T5;
+#endif
+#if ALDP_KEYS >= 1
+        const uint32_t x0 = fadd(faddc<T0>(a.r, one), b.r, one), x4 = fadd(faddc<T4>(a.l, one), b.l, one);
+#else
         const uint32_t x0 = a.r + b.r + T0, x4 = a.l + b.l + T4;   // + c.r / + c.l fused
+#endif
         const uint32_t x2 = a.lc + T2, x6 = c.lc + T6;             // + a.r / + c.r fused
         if constexpr (K == 4)
             return top4_id(vaddmax(x0, c.r, k1), vaddmin(x0, c.r, k1), vaddmax(x2, a.r, k3), vaddmin(x2, a.r, k3),
@@ -269,7 +298,7 @@ __device__ __forceinline__ void load_words(const uint8_t* p, uint32_t (&w)[NW]) 
 // real neighbours); a separate instantiation keeps the common path's row
 // clamp a compile-time [0, rows) (a runtime bound measured 1.8 % slower).
 template <int K, int NW, bool CELLS, bool CODES, bool HIST, bool HALO = false, int NC = kMaxTileCells>
-__global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_kernel(FastParams p) {
+__global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : ALDP_MINB) ldp_fast_kernel(FastParams p) {
     constexpr bool LBP = K == 0;
     constexpr int TS = fast_tag_set(CELLS);  // the host builds the id tables for the same set
     using Lay = FastLayout<K, NW, NC>;
@@ -286,6 +315,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
     constexpr int SUMS = CELLS ? ALDP_CELL_SUMS : 2;  // measured: all stored sums win only without cells
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ __align__(4) uint8_t id_bin[128];
+    __shared__ __align__(4) uint8_t bin_id[NARROW ? 64 : 4];
     __shared__ int fix_cols[kFastWarps][NSEG][Lay::FIX];
     __shared__ int fix_n[kFastWarps][NSEG];
 
@@ -311,6 +341,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
             w[i] = table ? uint32_t(p.id_code[NARROW ? in_region : in_region ^ slot_skew(sg, region)]) : 0u;
         }
         if (!LBP && threadIdx.x < NT) id_bin[threadIdx.x] = p.id_bin[threadIdx.x];
+        if (NARROW && threadIdx.x < 64) bin_id[threadIdx.x] = p.bin_id[threadIdx.x];
     }
     __syncthreads();
 
@@ -772,7 +803,49 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : 2) ldp_fast_ker
         __syncwarp();
 
         // ---- flush: one global atomic per (cell, bin) seen, then re-zero ----
-        if (HIST) {
+        if (HIST && NARROW && p.store_whole) {
+            // Narrow cells: a cell that lies wholly inside this tile is
+            // stored -- all its bins, zeros included, four per lane (lanes
+            // sl < NB / 4) -- so its histogram needs no memset and no global
+            // atomics; a cell that straddles the tile's edge adds its non-zero
+            // bins to the histogram zeroed beforehand. Then the tables are
+            // re-zeroed.
+            constexpr int NB = (K == 1 || K == 7) ? 8 : (K == 2 || K == 6) ? 28 : 56;
+            constexpr int G4 = NB / 4;
+            const uint8_t* seg_ptr = smem_al + (seg_base - smem_base);
+            const int c_end = min(c0 + kTileCols, min(p.cols, p.grid_c * p.cell_cols));
+            const int n_c = c_end > c0 ? (c_end - 1) / p.cell_cols - cell_c0 + 1 : 0;
+            if (do_hist && sl < G4) {
+                const uint32_t ids = reinterpret_cast<const uint32_t*>(bin_id)[sl];  // bins 4 sl .. 4 sl + 3
+                const int64_t at0 = ((int64_t(img) * p.grid_r + crow) * p.grid_c + cell_c0) * NB + 4 * sl;
+                for (int lc = 0; lc < n_c; ++lc) {
+                    const uint32_t* cnt = reinterpret_cast<const uint32_t*>(seg_ptr + lc * REGION + CNT);
+                    const uint32_t sk = slot_skew(seg, lc);
+                    uint32_t c4[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) c4[j] = cnt[((ids >> (8 * j)) & 0xFFu) ^ sk];
+                    const int cf = (cell_c0 + lc) * p.cell_cols;
+                    const bool whole = cf >= c0 && cf + p.cell_cols <= c0 + kTileCols;
+                    const int64_t at = at0 + int64_t(lc) * NB;  // bins; a multiple of 4
+                    if (whole) {
+                        if (!p.hist16)
+                            *reinterpret_cast<uint4*>(p.hist + at) = make_uint4(c4[0], c4[1], c4[2], c4[3]);
+                        else
+                            *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(p.hist) + at) =
+                                make_uint2(c4[0] | (c4[1] << 16), c4[2] | (c4[3] << 16));
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            if (c4[j]) hist_add(p.hist, p.hist16, at + j, c4[j]);
+                    }
+                }
+            }
+            __syncwarp();
+            uint4* tb = reinterpret_cast<uint4*>(smem_al + (seg_base - smem_base));
+            for (int j = sl; j < n_c * (REGION / 16); j += SEG) tb[j] = make_uint4(0u, 0u, 0u, 0u);
+            uint4* tr = reinterpret_cast<uint4*>(smem_al + (seg_base - smem_base) + NC * REGION + CNT);
+            for (int j = sl; j < NT / 4; j += SEG) tr[j] = make_uint4(0u, 0u, 0u, 0u);
+        } else if (HIST) {
             int ntab = 0;
             if (do_hist) {
                 if (CELLS) {

@@ -278,8 +278,41 @@ static aldp_status finish_fast(FastParams& p, int n_images, int cell_rows, int c
             if (p.id_code[id]) return fail(ALDP_EINVAL, "internal: code id collision");
             p.id_code[id] = uint8_t(c);
             p.id_bin[id] = uint8_t(colex_rank(c));
+            if (k != 4) p.bin_id[colex_rank(c)] = uint8_t(id);
         }
     return launch_fast(p, k, cells, narrow, halo, st);
+}
+
+// How the narrow-cell kernel writes its histograms (ALDP_NARROW_HIST
+// overrides, read per call so tests can toggle it):
+//   0 = every bin added with global atomics into a memset histogram (round 1);
+//   2 = cells wholly inside a 128-column tile stored, the few that straddle a
+//       tile edge added after zero_straddling_cells (default).
+// A/B on 2048 C5 frames (profiles/r02_narrow_ab.txt): window 10: 283 k -> 338 k
+// Mpixel/s, window 25: 501 k -> 522 k. (Mode 1, tiles of whole cells with
+// every bin stored, measured 301 k / 398 k and was dropped: its tiles
+// recompute the columns they overlap.)
+static int narrow_hist_mode() {
+    const char* e = std::getenv("ALDP_NARROW_HIST");
+    return e ? std::atoi(e) : 2;
+}
+
+// Zeroes the histograms of the cells that straddle a 128-column tile edge
+// (narrow mode 2 adds into those; every other cell is stored whole).
+__global__ void zero_straddling_cells(uint32_t* hist, int hist16, int64_t n_cells, int grid_c, int cell_cols,
+                                      int nbins) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n_cells;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int cf = int(i % grid_c) * cell_cols;
+        if (cf / kTileCols == (cf + cell_cols - 1) / kTileCols) continue;
+        if (hist16) {
+            uint16_t* h = reinterpret_cast<uint16_t*>(hist) + i * nbins;
+            for (int b = 0; b < nbins; ++b) h[b] = 0;
+        } else {
+            uint32_t* h = hist + i * nbins;
+            for (int b = 0; b < nbins; ++b) h[b] = 0;
+        }
+    }
 }
 
 // lbp: the LBP descriptor (256 bins, k ignored); internally k == 0.
@@ -296,11 +329,6 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
         if (area >= 65536) return fail(ALDP_EINVAL, "hist_u16: a histogram can reach 65536 counts");
         if (reinterpret_cast<uintptr_t>(a->d_hist) % 4) return fail(ALDP_EINVAL, "hist_u16: d_hist not 4-byte aligned");
     }
-    if (a->d_hist)
-        ALDP_CUDA_TRY(cudaMemsetAsync(a->d_hist, 0,
-                                      (a->hist_u16 ? 2 : 4) * size_t(a->n_images) * cells * nbins, st));
-    if (a->n_images == 0 || (!a->d_codes && !a->d_hist)) return ALDP_OK;
-
     const int al = 4 * kLaneWords;  // alignment the per-lane vector loads/stores need
     const bool aligned =
         a->pitch % al == 0 && (a->n_images <= 1 || a->img_stride % al == 0) &&
@@ -313,6 +341,24 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
     if (a->cell_rows && a->d_hist) ncl = max_cells_per_tile(a->cols, a->cell_cols, grid_c);
     const bool narrow = ncl > kMaxTileCells;
     const bool fast_ok = aligned && (!narrow || (ncl <= kNarrowTileCells && a->cell_cols >= 9 && !lbp && a->k != 4));
+    // narrow cells: histograms stored four bins at a time (16-byte stores of
+    // u32 bins, 8-byte of u16) -- mode 2 of narrow_hist_mode()
+    const int nmode = (kernel != ALDP_KERNEL_GENERIC && fast_ok && narrow && !a->cell_from_map &&
+                       reinterpret_cast<uintptr_t>(a->d_hist) % (a->hist_u16 ? 8 : 16) == 0)
+                          ? narrow_hist_mode()
+                          : 0;
+    if (a->d_hist && nmode == 0)
+        ALDP_CUDA_TRY(cudaMemsetAsync(a->d_hist, 0,
+                                      (a->hist_u16 ? 2 : 4) * size_t(a->n_images) * cells * nbins, st));
+    if (a->d_hist && nmode == 2 && a->n_images > 0) {
+        const int64_t n_cells = int64_t(a->n_images) * cells;
+        const int grid = int(std::min<int64_t>((n_cells + 255) / 256, 8LL * n_sms()));
+        zero_straddling_cells<<<grid, 256, 0, st>>>(a->d_hist, a->hist_u16, n_cells, grid_c, a->cell_cols, nbins);
+        count_launch();
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "zero_straddling_cells launch");
+    }
+    if (a->n_images == 0 || (!a->d_codes && !a->d_hist)) return ALDP_OK;
     if (kernel == ALDP_KERNEL_FAST && !fast_ok)
         return fail(ALDP_EINVAL, "fast kernel needs 8-byte aligned pitches/strides and at most 5 cells per "
                                  "128 columns (16 for LDP k != 4 with cells of >= 9 columns)");
@@ -340,6 +386,7 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
         p.grid_r = grid_r;
         p.grid_c = grid_c;
         p.blocks = (a->cols + kTileCols - 1) / kTileCols;
+        p.store_whole = nmode == 2 ? 1 : 0;
         // Cell histograms with rows below the cell grid (490 = 6 x 81 + 4 for
         // the 7x6 grid of a 640x490 frame): the grid rows run as one launch and
         // the short remainder as a second, codes-only launch. Warps take tiles
@@ -379,6 +426,8 @@ static aldp_status run_batch(const aldp_ldp_args* a, int kernel, cudaStream_t st
             q.rows = a->rows - start;
             q.codes = a->d_codes + int64_t(start) * a->codes_pitch;
             q.hist = nullptr;
+            q.store_whole = 0;
+            q.blocks = (a->cols + kTileCols - 1) / kTileCols;
             q.cell_rows = q.cell_cols = 0;
             q.grid_r = q.grid_c = 1;
             q.edge_lo = q.edge_hi = -1;

@@ -594,3 +594,29 @@ def test_narrow_cells_fallbacks():
             np.array_equal(h.cpu().numpy().astype(np.uint64), rh), (k, cell)
         with pytest.raises(ValueError):
             aldp.ldp_batch(px, 64, 160, k=k, cell=cell, codes=True, hist=True, kernel="fast")
+
+
+@pytest.mark.parametrize("own", ["0", "2"])
+@pytest.mark.parametrize("window", [9, 10, 12, 16, 20, 25, 31])
+def test_narrow_hist_modes(window, own, monkeypatch):
+    """Both ways the narrow-cell kernel writes histograms (ldp_kernels.cu
+    narrow_hist_mode, forced by ALDP_NARROW_HIST): 0 = global atomics into a
+    memset buffer, 2 = cells wholly inside a 128-column tile stored (every
+    bin, no memset) and the straddling ones added after a zeroing launch.
+    Output buffers pre-filled with garbage must come out exact; u32 and u16
+    histograms; frames with rows/columns beyond the cell grid and widths that
+    are not a multiple of 128."""
+    monkeypatch.setenv("ALDP_NARROW_HIST", own)
+    for n, r, c, seed in ((3, 2 * window + 5, 330, window), (2, 490, 640, 7 * window)):
+        px = aldp.gen_faces(n, r, c, blobs=8, seed=seed, device=DEV)
+        host = px[:, :, :c].cpu().numpy()
+        rc, rh = oracle.batch(host, k=3, cell=(window, window))
+        cells = rh.shape[1]
+        for dt in (torch.int32, torch.int16):
+            codes = torch.full((n, r, px.shape[2]), 0xA5, dtype=torch.uint8, device=DEV)
+            hist = torch.full((n, cells, 56), 12345, dtype=dt, device=DEV)
+            aldp.ldp_batch(px, r, c, k=3, cell=(window, window), codes=codes, hist=hist, kernel="fast")
+            torch.cuda.synchronize()
+            assert np.array_equal(codes[:, :, :c].cpu().numpy(), rc), (window, own, dt)
+            got = hist.cpu().numpy().astype(np.int64) & (0xFFFF if dt == torch.int16 else -1)
+            assert np.array_equal(got.astype(np.uint64), rh), (window, own, dt)
