@@ -69,6 +69,9 @@ struct FastLayout {
     static constexpr int FIX = NARROW ? 2 * NC + 2 : kFixList;          // border columns per segment
 };
 
+#ifndef ALDP_PROBE
+#define ALDP_PROBE 0  // 1: drop the row loop's code lookup and count (wrong output; ceiling probe)
+#endif
 #ifndef ALDP_MINB
 #define ALDP_MINB 2  // CTAs per SM the register allocation targets (NW = 2)
 #endif
@@ -623,7 +626,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : ALDP_MINB) ldp_
                         for (int s = 0; s < LC; ++s) e[s] = lds32(cd[s]);
                     } else {
 #pragma unroll
-                        for (int s = 0; s < LC; ++s) e[s] = lds32(ad[s] - CNT);
+                        for (int s = 0; s < LC; ++s) e[s] = ALDP_PROBE ? ad[s] & 0xFFu : lds32(ad[s] - CNT);
                     }
 #pragma unroll
                     for (int j = 0; j < NW; ++j)  // bytes -> word with multiply-adds (FMA pipe)
@@ -644,7 +647,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : ALDP_MINB) ldp_
                     addrs(Y, bd);
                     if (live) count(bd);
                 } else if (live) {
-                    count(ad);
+                    if (!ALDP_PROBE) count(ad);
                 }
             }
         };
