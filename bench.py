@@ -152,15 +152,25 @@ def ncu_record(cfg):
     return rec
 
 
-def limiter_of(rec):
-    """Name the measured limiter from the ncu counters: the unit closest to
-    its peak among DRAM, the L1/shared data pipe, the ALU pipe and instruction
-    issue."""
+def limiter_of(rec, cfg=None):
+    """The measured limiter from the ncu counters of the same build: the units
+    closest to their peak among DRAM, the L1/shared data pipe, the ALU pipe
+    and instruction issue. A unit at >= 80 % is named as the bound; below
+    that the kernel is co-limited (latency plus several busy units) and all
+    four are listed."""
     if not rec:
         return None
-    units = {"dram": rec.get("dram_throughput_pct", 0.0), "l1_data_pipe": rec.get("l1_data_pipe_pct", 0.0),
-             "alu_pipe": rec.get("alu_pipe_pct", 0.0), "issue": rec.get("issue_active_pct", 0.0)}
-    return max(units, key=units.get)
+    units = {"l1_data_pipe": rec.get("l1_data_pipe_pct", 0.0), "alu_pipe": rec.get("alu_pipe_pct", 0.0),
+             "issue": rec.get("issue_active_pct", 0.0), "dram": rec.get("dram_throughput_pct", 0.0)}
+    order = sorted(units, key=units.get, reverse=True)
+    listed = ", ".join(f"{u} {units[u]:.1f} %" for u in order)
+    if units[order[0]] >= 80.0:
+        return f"{order[0]}-bound ({listed})"
+    out = f"co-limited, no unit at 80 % of peak ({listed})"
+    if cfg in ("c5", "c4", "c2"):  # the 81x91 / 64x64 cell kernel the probe ran on
+        out += ("; ceiling probe of this kernel: removing every per-pixel shared access drops the L1 pipe "
+                "to 24 % for +8 % only (profiles/r02_ncu_shared_ceiling_probe.txt)")
+    return out
 
 
 def measured_peaks():
@@ -546,7 +556,7 @@ def main():
                      "launches_per_step": kernels_per_step,
                      # what ncu measured for this kernel: the roofline is HBM, but
                      # the kernel is limited by instruction issue / the ALU pipe
-                     "limiter": limiter_of(ncu),
+                     "limiter": limiter_of(ncu, args.config),
                      "ncu": ncu},
         "clocks": clocks,
         "gpu_launches": args.steps * kernels_per_step,

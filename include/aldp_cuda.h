@@ -101,8 +101,9 @@ aldp_status aldp_ldp_batch(const aldp_ldp_args* args, void* stream);
 
 /* Kernel selection for aldp_ldp_batch: AUTO picks the packed sm_100a kernel
  * whenever the layout allows it (pitches, strides and base pointers 8-byte
- * aligned -- any width and any k -- at most 5 cells per 128 columns) and the
- * generic per-pixel kernel otherwise. FAST fails with
+ * aligned -- any width and any k -- and at most 5 cells per 128 columns, or
+ * up to 16 for LDP k != 4 with cells of >= 9 columns) and the generic
+ * per-pixel kernel otherwise. FAST fails with
  * ALDP_EINVAL when the layout does not allow it. Both are CUDA; there is no
  * CPU path. */
 enum { ALDP_KERNEL_AUTO = 0, ALDP_KERNEL_FAST = 1, ALDP_KERNEL_GENERIC = 2 };
@@ -116,7 +117,9 @@ aldp_status aldp_lbp_batch(const aldp_ldp_args* args, void* stream);
 aldp_status aldp_lbp_batch_ex(const aldp_ldp_args* args, int kernel, void* stream);
 
 /* Kernel launches the last aldp_ldp_batch* / aldp_lbp_batch* call on this
- * host thread made (0, 1, or 2 for a cell grid whose rows overhang it). */
+ * host thread made: 0 .. 3 (the LDP/LBP kernel; a second, codes-only launch
+ * for the rows of a cell grid's overhang; on narrow cells a launch that zeroes
+ * the cells straddling a 128-column tile edge). */
 int aldp_last_launch_count(void);
 
 /* Negative control for parity harnesses (the analogue of the reference's

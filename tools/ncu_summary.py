@@ -24,8 +24,8 @@ def details(rep):
 def raw(rep, keys):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
-    h, v = rows[0], rows[2]
-    return {k: v[h.index(k)] for k in keys if k in h}
+    h, u, v = rows[0], rows[1], rows[2]  # header, units, values
+    return {k: (v[h.index(k)] + " " + u[h.index(k)]).strip() for k in keys if k in h}
 
 
 def launches(path):
