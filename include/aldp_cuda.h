@@ -62,8 +62,12 @@ enum { ALDP_DESC_LBP = 2 };
  *  d_codes     nullable. Code map, whole-image clamp (the per-pixel code of
  *              descriptors.cpp:129-136), row pitch codes_pitch, image stride
  *              codes_img_stride.
- *  d_hist      nullable. uint32 [n_images][grid_cells][aldp_n_bins(k)];
- *              overwritten (zeroed by the call, stream-ordered).
+ *  d_hist      nullable. uint32 [n_images][grid_cells][aldp_n_bins(k)]
+ *              (uint16 with hist_u16); every bin is overwritten, stream-ordered
+ *              (a memset, or on narrow cells whole-cell stores plus a zeroing
+ *              launch for the cells that straddle a 128-column tile). Narrow
+ *              cells store 16 bytes at a time: d_hist 16-byte aligned (8 for
+ *              uint16) keeps that path, otherwise the memset + atomics path.
  *
  * Asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream).
  * No hidden allocation; caller owns every buffer. */
