@@ -102,6 +102,7 @@ struct FastParams {
     uint64_t mg_group, mg_bandG, mg_band1, mg_blocks, mg_cell;
     int sh_group, sh_bandG, sh_band1, sh_blocks, sh_cell;
     int band_rows, bands, blocks;
+    int uniform_bands;  // rows is a multiple of band_rows: no band is shorter
     int64_t n_tiles;
     // narrow cells: store the cells wholly inside a tile, add the ones that
     // straddle a tile edge (zeroed beforehand by zero_straddling_cells)
@@ -407,7 +408,11 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : ALDP_MINB) ldp_
         const int seg_rows = seg_live ? band_h : 0;
         // warp-wide row count from warp-uniform quantities only (no shuffle),
         // so the row loop's trip count is known uniform
-        int n_rows = 0;
+        // (every band band_rows tall -- the cell grid's launch -- needs no
+        // look at the other segment's tile: A/B C5 +0.9 %, window 10 / 25 +2 %)
+        int n_rows = p.band_rows;
+        if (!p.uniform_bands) {
+        n_rows = 0;
 #pragma unroll
         for (int sg = 0; sg < NSEG; ++sg) {
             const int64_t tt = NSEG * wt + sg;
@@ -417,6 +422,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, NW == 1 ? 3 : ALDP_MINB) ldp_
                 band_geom(bnd, r0_, h_, cr_);
                 n_rows = max(n_rows, h_);
             }
+        }
         }
         const int c0 = blk * kTileCols;
         const int y = c0 + sl * LC;

@@ -259,6 +259,7 @@ static aldp_status finish_fast(FastParams& p, int n_images, int cell_rows, int c
             p.band_rows /= 2;
     }
     p.bands = (p.rows + p.band_rows - 1) / p.band_rows;
+    p.uniform_bands = p.rows % p.band_rows == 0 ? 1 : 0;
     p.n_tiles = int64_t(n_images) * p.bands * p.blocks;
     {
         const int G = (p.blocks & 1) ? 2 : 1;
