@@ -531,7 +531,10 @@ def test_small_batch_split_launch(k, rows, cell):
     tall = f[:, :, :cols].cpu().numpy()
     # plain frames: the first `rows` rows of each tall frame (k = 0: LBP)
     px = tall[:, :rows]
-    codes, hist = aldp.ldp_batch(to_dev(px), rows, cols, k=k, cell=cell, codes=True, hist=True)
+    # kernel="fast": these layouts must take the packed kernel and its split
+    # launch (grid rows, then the remainder rows), never the generic kernel
+    codes, hist = aldp.ldp_batch(to_dev(px), rows, cols, k=k, cell=cell, codes=True, hist=True, kernel="fast")
+    assert aldp.last_launch_count() == 2, (k, rows, cell)
     torch.cuda.synchronize()
     want_c, want_h = oracle.batch(px, k=k, cell=cell)
     assert np.array_equal(codes[:, :, :cols].cpu().numpy(), want_c), (k, rows, cell)
@@ -539,7 +542,8 @@ def test_small_batch_split_launch(k, rows, cell):
     # band view: rows 1 .. rows of one tall frame, real rows above and below
     dt = to_dev(tall[0])
     view = dt[:, 1:rows + 1, :]
-    codes, hist = aldp.ldp_batch(view, rows, cols, k=k, cell=cell, codes=True, hist=True, halo=(1, 1))
+    codes, hist = aldp.ldp_batch(view, rows, cols, k=k, cell=cell, codes=True, hist=True, halo=(1, 1),
+                                 kernel="fast")
     torch.cuda.synchronize()
     full_c, _ = oracle.batch(tall[:1], k=k, hist=False)
     assert np.array_equal(codes[0, :, :cols].cpu().numpy(), full_c[0, 1:rows + 1]), (k, rows, cell)
