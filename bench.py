@@ -148,7 +148,12 @@ def ncu_record(cfg):
     except OSError:
         sha = None
     rec = dict(rec)
-    rec["same_build"] = sha is not None and sha == rec.get("lib_sha256")
+    # same device code as the capture: the sm_100a sections of the embedded
+    # cubins (a rebuild of identical code changes the .so's bytes -- nvcc's
+    # temporary names in the debug strings -- but not these)
+    code = aldp.device_code_fingerprint()
+    rec["same_build"] = bool((code is not None and code == rec.get("device_code_sha256")) or
+                             (sha is not None and sha == rec.get("lib_sha256")))
     return rec
 
 

@@ -173,6 +173,44 @@ def _check(status: int) -> None:
         raise _STATUS_EXC.get(status, AldpError)(msg)
 
 
+def device_code_fingerprint(lib_path: Optional[str] = None) -> Optional[str]:
+    """sha256 over the sm_100a code of a library build: every section of
+    every embedded cubin except the debug-string sections (which carry nvcc's
+    temporary file names, so rebuilding identical code changes the .so's own
+    sha256 but not this). None when cuobjdump is unavailable."""
+    import hashlib
+    import shutil
+    import struct
+    import subprocess
+    import tempfile
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        return None
+    h = hashlib.sha256()
+    with tempfile.TemporaryDirectory() as d:
+        r = subprocess.run([tool, "-xelf", "all", os.path.abspath(lib_path or LIB_PATH)], cwd=d,
+                           capture_output=True)
+        if r.returncode != 0:
+            return None
+        for name in sorted(os.listdir(d)):
+            b = open(os.path.join(d, name), "rb").read()
+            if b[:4] != b"\x7fELF" or b[4] != 2:
+                continue
+            shoff = struct.unpack_from("<Q", b, 0x28)[0]
+            shentsize, shnum, shstrndx = struct.unpack_from("<HHH", b, 0x3A)
+            hdrs = [struct.unpack_from("<IIQQQQIIQQ", b, shoff + i * shentsize) for i in range(shnum)]
+            strtab = hdrs[shstrndx][4]
+            h.update(name.encode())
+            for sh in hdrs:
+                sec = b[strtab + sh[0]:b.index(b"\0", strtab + sh[0])]
+                if b"debug" in sec:
+                    continue
+                h.update(sec)
+                if sh[1] != 8:  # SHT_NOBITS has no bytes in the file
+                    h.update(b[sh[4]:sh[4] + sh[5]])
+    return h.hexdigest()
+
+
 def version() -> str:
     return lib.aldp_version().decode()
 

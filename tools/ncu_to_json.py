@@ -13,8 +13,11 @@ import io
 import json
 import os
 import subprocess
+import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_1810_11518_b200 import device_code_fingerprint  # noqa: E402
 
 
 def raw(rep):
@@ -67,6 +70,7 @@ def main():
         "pixels_per_launch": px,
         "source": os.path.relpath(os.path.abspath(a.rep), ROOT),
         "lib_sha256": hashlib.sha256(open(a.lib, "rb").read()).hexdigest(),
+        "device_code_sha256": device_code_fingerprint(a.lib),
     }
     db = {}
     if os.path.exists(a.out):
