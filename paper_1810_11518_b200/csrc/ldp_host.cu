@@ -9,6 +9,9 @@
 //   aldp_ldp_code_map       <- new (descriptors.cpp:129-136 per-pixel code)
 //   aldp_ldp_batch_host     <- batch of the above (end-to-end bench path)
 #include <cuda_runtime.h>
+#if defined(__x86_64__) || defined(_M_X64)
+#include <emmintrin.h>
+#endif
 
 #include <algorithm>
 #include <cmath>
@@ -148,16 +151,60 @@ static bool is_pinned(const void* p) {
     return at.type == cudaMemoryTypeHost;
 }
 
+// Large copy with non-temporal (streaming) stores: the staging and caller
+// buffers it fills are read next by the DMA engine or much later by the
+// caller, so write-allocating them in the host caches only costs memory
+// bandwidth -- the resource the pageable path is bound by. SSE2 only (any
+// x86-64 host). ALDP_NT_COPY=0 turns it off (A/B).
+static bool nt_copy_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("ALDP_NT_COPY");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+static void copy_bytes(uint8_t* dst, const uint8_t* src, size_t n) {
+#if defined(__x86_64__) || defined(_M_X64)
+    if (n >= (size_t(1) << 16) && nt_copy_enabled()) {
+        const size_t head = (16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15;
+        std::memcpy(dst, src, head);
+        dst += head, src += head, n -= head;
+        const size_t body = n & ~size_t(63);
+        for (size_t i = 0; i < body; i += 64) {
+            const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i));
+            const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 16));
+            const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 32));
+            const __m128i d = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 48));
+            _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), a);
+            _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 16), b);
+            _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 32), c);
+            _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 48), d);
+        }
+        std::memcpy(dst + body, src + body, n - body);
+        _mm_sfence();  // streaming stores drained before the buffer is handed on
+        return;
+    }
+#endif
+    std::memcpy(dst, src, n);
+}
+
 // Copies `nrows` rows of `width` bytes between strided buffers on up to
 // kCopyThreads host threads (one thread moves ~8 GB/s; PCIe needs ~45).
-constexpr int kCopyThreads = 8;
+constexpr int kCopyThreads = 16;
+static int copy_threads() {
+    static const int t = [] {
+        const char* e = std::getenv("ALDP_COPY_THREADS");
+        return e ? std::max(1, std::min(kCopyThreads, std::atoi(e))) : 8;
+    }();
+    return t;
+}
 static void copy_rows(uint8_t* dst, size_t dst_pitch, const uint8_t* src, size_t src_pitch, size_t width,
                       size_t nrows) {
     const size_t bytes = width * nrows;
-    const int t = int(std::min<size_t>(kCopyThreads, std::max<size_t>(1, bytes >> 22)));  // >= 4 MB per thread
+    const int t = int(std::min<size_t>(copy_threads(), std::max<size_t>(1, bytes >> 22)));  // >= 4 MB per thread
     auto part = [&](size_t r0, size_t r1) {
         if (dst_pitch == width && src_pitch == width) {
-            std::memcpy(dst + r0 * width, src + r0 * width, (r1 - r0) * width);
+            copy_bytes(dst + r0 * width, src + r0 * width, (r1 - r0) * width);
         } else {
             for (size_t r = r0; r < r1; ++r) std::memcpy(dst + r * dst_pitch, src + r * src_pitch, width);
         }
