@@ -154,3 +154,32 @@ def test_calls_without_gpu_report_cuda_error():
         aldp.ldp_histogram(np.zeros((8, 8), np.uint8), k=2)
     with pytest.raises(ValueError):
         aldp.ldp_code_map(np.zeros((2, 8), np.uint8))
+
+
+def test_device_code_fingerprint_is_stable():
+    """bench.py matches the committed ncu record to the library it loads by
+    the fingerprint of the sm_100a code (cubin sections without the debug
+    strings), which -- unlike the .so's own sha256 -- survives a rebuild of
+    the same code."""
+    import hashlib
+    import shutil
+    import paper_1810_11518_b200 as aldp
+    if not (shutil.which("cuobjdump") or os.path.exists("/usr/local/cuda/bin/cuobjdump")):
+        pytest.skip("cuobjdump not available")
+    a, b = aldp.device_code_fingerprint(), aldp.device_code_fingerprint()
+    assert a == b and re.fullmatch(r"[0-9a-f]{64}", a)
+    assert a != hashlib.sha256(open(aldp.LIB_PATH, "rb").read()).hexdigest()
+
+
+def test_bench_limiter_statement():
+    """The bench line names a bound only when a unit reaches 80 % of its peak;
+    otherwise it lists the units as co-limited (ncu counters)."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import bench
+    rec = {"l1_data_pipe_pct": 73.1, "alu_pipe_pct": 66.7, "issue_active_pct": 64.7, "dram_throughput_pct": 22.2}
+    s = bench.limiter_of(rec, "c5")
+    assert s.startswith("co-limited") and "l1_data_pipe 73.1 %" in s and "ceiling probe" in s
+    assert "ceiling probe" not in bench.limiter_of(rec, "w10")
+    assert bench.limiter_of(dict(rec, dram_throughput_pct=85.0)).startswith("dram-bound")
+    assert bench.limiter_of(None) is None
