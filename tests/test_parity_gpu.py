@@ -624,3 +624,21 @@ def test_narrow_hist_modes(window, own, monkeypatch):
             assert np.array_equal(codes[:, :, :c].cpu().numpy(), rc), (window, own, dt)
             got = hist.cpu().numpy().astype(np.int64) & (0xFFFF if dt == torch.int16 else -1)
             assert np.array_equal(got.astype(np.uint64), rh), (window, own, dt)
+
+
+def test_narrow_hist_unaligned_buffer_falls_back():
+    """Narrow cells store whole cells 16 bytes at a time (8 for uint16 bins);
+    a histogram buffer that is only 4-byte aligned takes the memset + atomics
+    path instead and must give the same bits."""
+    px = aldp.gen_faces(2, 200, 330, blobs=8, seed=5, device=DEV)
+    host = px[:, :, :330].cpu().numpy()
+    _, rh = oracle.batch(host, k=3, cell=(10, 10), codes=False)
+    cells = rh.shape[1]
+    for dt, off in ((torch.int32, 1), (torch.int32, 2), (torch.int16, 2)):
+        buf = torch.full((2 * cells * 56 + off,), 999, dtype=dt, device=DEV)
+        hist = buf[off:].view(2, cells, 56)  # base 4 or 8 bytes (int32) / 4 bytes (int16) past 16-byte alignment
+        aldp.ldp_batch(px, 200, 330, k=3, cell=(10, 10), hist=hist, kernel="fast")
+        torch.cuda.synchronize()
+        got = hist.cpu().numpy().astype(np.int64) & (0xFFFF if dt == torch.int16 else -1)
+        assert np.array_equal(got.astype(np.uint64), rh), (dt, off)
+        assert int(buf[:off].max()) == 999  # nothing written before the buffer
