@@ -69,6 +69,9 @@ struct FastLayout {
     static constexpr int FIX = NARROW ? 2 * NC + 2 : kFixList;          // border columns per segment
 };
 
+#ifndef ALDP_PIXEL_LAYER
+#define ALDP_PIXEL_LAYER 1  // first comparator layer on single pixels (pair_id); 0 = keys formed first (round 1)
+#endif
 #ifndef ALDP_PROBE
 #define ALDP_PROBE 0  // 1: drop the row loop's code lookup and count (wrong output; ceiling probe)
 #endif
@@ -162,6 +165,53 @@ __device__ __forceinline__ uint32_t pair_id(const Col& a, const Col& b, const Co
     constexpr uint32_t T0 = kTagT<TS>(0) * 0x10001u, T1 = kTagT<TS>(1) * 0x10001u, T2 = kTagT<TS>(2) * 0x10001u,
                        T3 = kTagT<TS>(3) * 0x10001u, T4 = kTagT<TS>(4) * 0x10001u, T5 = kTagT<TS>(5) * 0x10001u,
                        T6 = kTagT<TS>(6) * 0x10001u, T7 = kTagT<TS>(7) * 0x10001u;
+#if ALDP_PIXEL_LAYER
+    if constexpr (K != 4) {
+        // First comparator layer on single pixels (round 2, the kept key
+        // scheme). The paired keys share two ring pixels (K0/K1: TR+R, K2/K3:
+        // TL+T, K4/K5: BL+L, K6/K7: BR+B) and differ in one, so
+        //   max/min(K_2i, K_2i+1) = C_i + max/min(u + D_i, v),
+        // D_i = W[2i] - W[2i+1] > 0, C_i = the shared pair + W[2i+1]. No key
+        // is formed before the layer: its eight VIADDMNMX take pixel operands
+        // and the tag difference as the immediate add. The shared sums and the
+        // adds that complete the maxima run on the FMA pipe (IMAD); for k == 3
+        // each half's minima meet only in max(q, s), so one of them rides that
+        // comparator's add. Row loop: 22 ALU-pipe instructions per pair
+        // instead of 27 (the ALU pipe, which runs every min/max, is what the
+        // kernel waits on: an ALU instruction costs ~2.8 FMA-pipe ones in the
+        // A/B series, profiles/r02m_pixel_layer_ab.txt). The cell kernel
+        // (sums on use) forms the horizontal sums on the FMA pipe too; the
+        // whole-image kernel adds the tag to its stored row sums.
+        constexpr uint32_t D01 = T0 - T1, D23 = T2 - T3, D45 = T4 - T5, D67 = T6 - T7;
+        const uint32_t C01 = fadd(faddc<T1>(a.r, one), b.r, one), C45 = fadd(faddc<T5>(c.l, one), b.l, one);
+        uint32_t C23, C67;
+        if constexpr (TS == 0) {
+            C23 = fadd(faddc<T3>(a.l, one), a.c, one);
+            C67 = fadd(faddc<T7>(c.r, one), c.c, one);
+        } else {
+            C23 = a.lc + T3;
+            C67 = c.cr + T7;
+        }
+        const uint32_t M01 = vaddmax(c.r, D01, a.c), m01 = vaddmin(c.r, D01, a.c);
+        const uint32_t M23 = vaddmax(a.r, D23, b.l), m23 = vaddmin(a.r, D23, b.l);
+        const uint32_t M45 = vaddmax(a.l, D45, c.c), m45 = vaddmin(a.l, D45, c.c);
+        const uint32_t M67 = vaddmax(c.l, D67, b.r), m67 = vaddmin(c.l, D67, b.r);
+        const uint32_t pA = fadd(M01, C01, one), rA = fadd(M23, C23, one);
+        const uint32_t pB = fadd(M45, C45, one), rB = fadd(M67, C67, one);
+        const uint32_t sA = fadd(m23, C23, one), sB = fadd(m67, C67, one);
+        if constexpr (K == 3) {
+            const uint32_t yA = vaddmax(m01, C01, sA), yB = vaddmax(m45, C45, sB);  // max(q, s)
+            const uint32_t xA = vmin(pA, rA), xB = vmin(pB, rB);
+            const uint32_t a3 = vmin(xA, yA), b3 = vmin(xB, yB);
+            const uint32_t c1 = vmax3(pA, rA, b3);
+            const uint32_t c2 = vmax3(xA, yA, vmax(xB, yB));
+            const uint32_t c3 = vmax3(a3, pB, rB);
+            return c1 ^ c2 ^ c3;
+        } else {
+            return topk_from_pairs<K, TS>(pA, fadd(m01, C01, one), rA, sA, pB, fadd(m45, C45, one), rB, sB);
+        }
+    } else
+#endif
     if constexpr (TS == 1) {
         // Tag set 1 (the whole-image kernel; A/B: +6 % on C3, -5.9 % if used
         // by the cell kernel): the first-layer pairs share a two-input
