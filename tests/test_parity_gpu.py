@@ -121,6 +121,23 @@ def test_cell_histograms(cell):
         assert np.array_equal(h, want_h), (cell, kern)
 
 
+@pytest.mark.parametrize("rows,cell", [(300, (127, 91)), (300, (128, 64)), (300, (129, 40)), (300, (131, 130)),
+                                       (420, (257, 91)), (530, (260, 13)), (400, (400, 200))])
+@pytest.mark.parametrize("k", [3, 0])
+def test_tall_cell_rows(rows, cell, k):
+    """Cell rows taller than one staged halo chunk (130 rows incl. the two
+    neighbour rows): the row loop refills the tile's halo columns at 126-row
+    boundaries, in the unrolled loop or in its tail. LDP and LBP, regular and
+    narrow cells, rows below the grid."""
+    rng = np.random.default_rng(rows * 7 + cell[0])
+    img = rng.integers(0, 256, size=(2, rows, 300), dtype=np.uint8)
+    img[1, :, 120:140] = 7  # flat columns across a tile edge: ties in the halo columns
+    want_c, want_h = oracle.batch(img, k=k, cell=cell)
+    c, h = run(img, k, cell=cell, kernel="auto" if k == 0 and cell[1] < 26 else "fast")  # narrow cells: LDP only
+    assert np.array_equal(c, want_c), (rows, cell, k)
+    assert np.array_equal(h, want_h), (rows, cell, k)
+
+
 def test_cell_histograms_k_sweep():
     px = aldp.gen_faces(2, 162, 184, blobs=8, seed=3, device=DEV)
     torch.cuda.synchronize()
