@@ -21,7 +21,7 @@ far exceed L2 (126 MB), so no L2 flush is needed between steps.
             every rank at once through its own PCIe link, max over ranks
   roofline: algorithmic bytes (1 B in + 1 B code + 4 B x 42 x 56 hist per image)
             per launch / average launch time, vs MEASURED_PEAKS.json hbm_gbs;
-            traffic = ncu DRAM bytes per pixel (profiles/traffic.json) at that rate
+            traffic = ncu DRAM bytes per pixel (profiles/ncu_metrics.json, same build) at that rate
   clocks  : nvidia-smi samples during the timed region
   checksums: bin-weighted histogram sum and code-byte sum (identical at any N)
   cpu_baseline: the reference library (oracle/_ref, unmodified reference

@@ -14,8 +14,10 @@
 // pair "P_B" has (A, B, R), where L/R are A/B shifted by one column (one byte
 // permute from the neighbouring register; segment edges get their neighbour
 // through a rotating shuffle and one halo load). Pixel values are pre-scaled
-// by 64 so every key K_i = 64*S_i + W[i] is one 3-input add with its tag
-// (ldp_common.cuh).
+// by 64, so a key K_i = 64*S_i + W[i] (ldp_common.cuh) is a sum of three
+// pixel registers and its tag; pair_id never forms the eight keys: the first
+// comparator layer compares the one pixel in which two neighbouring
+// directions differ and adds the two they share afterwards.
 //
 // Histograms: per warp, per segment, one 64-entry u32 table per cell the
 // tile touches, counted by RED.shared.add (B200 serves same-address shared
@@ -176,12 +178,15 @@ __device__ __forceinline__ uint32_t pair_id(const Col& a, const Col& b, const Co
         // and the tag difference as the immediate add. The shared sums and the
         // adds that complete the maxima run on the FMA pipe (IMAD); for k == 3
         // each half's minima meet only in max(q, s), so one of them rides that
-        // comparator's add. Row loop: 22 ALU-pipe instructions per pair
-        // instead of 27 (the ALU pipe, which runs every min/max, is what the
-        // kernel waits on: an ALU instruction costs ~2.8 FMA-pipe ones in the
-        // A/B series, profiles/r02m_pixel_layer_ab.txt). The cell kernel
-        // (sums on use) forms the horizontal sums on the FMA pipe too; the
-        // whole-image kernel adds the tag to its stored row sums.
+        // comparator's add. The row loop's ALU-pipe instructions drop from
+        // 324 to 300 per 24 pixels at the same total (the ALU pipe, which runs
+        // every min/max, is what the kernel waits on: an ALU instruction costs
+        // ~2.8 FMA-pipe ones in the A/B series,
+        // profiles/r02m_pixel_layer_ab.txt). The cell kernel (sums on use)
+        // forms the horizontal sums on the FMA pipe too; the whole-image
+        // kernel adds the tag to its stored row sums. k == 4 keeps the keys
+        // formed first (top4_id needs K0 itself; this layer measured 1 %
+        // slower there).
         constexpr uint32_t D01 = T0 - T1, D23 = T2 - T3, D45 = T4 - T5, D67 = T6 - T7;
         const uint32_t C01 = fadd(faddc<T1>(a.r, one), b.r, one), C45 = fadd(faddc<T5>(c.l, one), b.l, one);
         uint32_t C23, C67;
