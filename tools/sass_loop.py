@@ -44,7 +44,7 @@ def main(lib, key):
         # the 3-way unrolled row loop: the smallest loop with 24 shared atomics (8 pixels x 3 rows per lane)
         def n(l, op):
             return sum(op in t for a, t in ins if l[0] <= a <= l[1])
-        lo, hi = min((l for l in loops if n(l, 'ATOMS') >= 24 and n(l, 'STG') >= 3), key=lambda l: l[1] - l[0])
+        lo, hi = min((l for l in loops if n(l, 'ATOMS') >= 24 and n(l, 'LDG') >= 3), key=lambda l: l[1] - l[0])
     body = [t for a, t in ins if lo <= a <= hi]
     c = collections.Counter(re.sub(r"^@!?U?P\d+\s+", "", t).split()[0].split(".")[0] for t in body)
     alu = {"VIMNMX", "VIMNMX3", "VIADDMNMX", "LOP3", "PRMT", "IADD3", "SHF", "SEL", "LEA", "ISETP", "IADD", "VIADD", "MOV"}
