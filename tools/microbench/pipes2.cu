@@ -27,6 +27,9 @@ __device__ __forceinline__ unsigned op(int k, unsigned a, unsigned b) {
     case 14: asm volatile("mad.lo.u32 %0, %1, %3, %2;" : "=r"(r) : "r"(a), "r"(b), "r"(b >> 31 | 1u)); break; // IMAD x*reg+y
     case 15: asm volatile("xor.b32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b)); break;             // LOP3
     case 16: asm volatile("mul.hi.u32 %0, %1, 0x40000;" : "=r"(r) : "r"(a)); r ^= b & 0; break; // IMAD.HI
+    case 17: asm volatile("set.ge.f16x2.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b)); break;  // HSET2.BF
+    case 18: asm volatile("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(0x44004400u), "r"(b)); break;  // HFMA2
+    case 19: asm volatile("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b | 0x40000u)); break;  // IMAD.HI reg
     default: r = a;
     }
     return r;
@@ -101,5 +104,13 @@ int main() {
     run("IMAD reg-1 + VIMNMX", probe<14, 0>);
     run("IMAD.HI + VIMNMX", probe<16, 0>);
     run("XOR + IMAD", probe<15, 1>);
+    run("HSET2", probe<17, 17>);
+    run("HSET2 + VIMNMX", probe<17, 0>);
+    run("HSET2 + IMAD", probe<17, 1>);
+    run("HFMA2", probe<18, 18>);
+    run("HFMA2 + VIMNMX", probe<18, 0>);
+    run("HSET2 + HFMA2", probe<17, 18>);
+    run("IMAD.HI", probe<16, 16>);
+    run("IMAD.HI + IMAD", probe<16, 1>);
     return 0;
 }
