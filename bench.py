@@ -161,8 +161,8 @@ def limiter_of(rec, cfg=None):
     """The measured limiter from the ncu counters of the same build: the units
     closest to their peak among DRAM, the L1/shared data pipe, the ALU pipe
     and instruction issue. A unit at >= 80 % is named as the bound; below
-    that the kernel is co-limited (latency plus several busy units) and all
-    four are listed."""
+    that all four are listed, with what the A/B series of the cell kernel
+    says it waits on."""
     if not rec:
         return None
     units = {"l1_data_pipe": rec.get("l1_data_pipe_pct", 0.0), "alu_pipe": rec.get("alu_pipe_pct", 0.0),
@@ -171,10 +171,13 @@ def limiter_of(rec, cfg=None):
     listed = ", ".join(f"{u} {units[u]:.1f} %" for u in order)
     if units[order[0]] >= 80.0:
         return f"{order[0]}-bound ({listed})"
-    out = f"co-limited, no unit at 80 % of peak ({listed})"
-    if cfg in ("c5", "c4", "c2"):  # the 81x91 / 64x64 cell kernel the probe ran on
-        out += ("; ceiling probe of this kernel: removing every per-pixel shared access drops the L1 pipe "
-                "to 24 % for +8 % only (profiles/r02_ncu_shared_ceiling_probe.txt)")
+    out = f"no unit at 80 % of peak ({listed})"
+    if cfg in ("c5", "c4", "c2"):  # the 81x91 / 64x64 cell kernel the A/B series and the probe ran on
+        out += ("; A/B of this kernel's key formation prices one ALU-pipe instruction at ~2.8 FMA-pipe ones "
+                "(profiles/r02m_pixel_layer_ab.txt): it waits on the ALU pipe, which runs every min/max of the "
+                "top-3 network (that network alone, on a 100 % busy ALU pipe, caps at 64 % of HBM); removing every "
+                "per-pixel shared access drops the L1 pipe to 24 % for +8 % only "
+                "(profiles/r02_ncu_shared_ceiling_probe.txt)")
     return out
 
 

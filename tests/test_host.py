@@ -173,13 +173,14 @@ def test_device_code_fingerprint_is_stable():
 
 def test_bench_limiter_statement():
     """The bench line names a bound only when a unit reaches 80 % of its peak;
-    otherwise it lists the units as co-limited (ncu counters)."""
+    otherwise it lists the units (ncu counters) and, for the
+    cell kernel, what the A/B series and the probe say it waits on."""
     import sys
     sys.path.insert(0, ROOT)
     import bench
     rec = {"l1_data_pipe_pct": 73.1, "alu_pipe_pct": 66.7, "issue_active_pct": 64.7, "dram_throughput_pct": 22.2}
     s = bench.limiter_of(rec, "c5")
-    assert s.startswith("co-limited") and "l1_data_pipe 73.1 %" in s and "ceiling probe" in s
-    assert "ceiling probe" not in bench.limiter_of(rec, "w10")
+    assert s.startswith("no unit at 80 %") and "l1_data_pipe 73.1 %" in s and "ALU pipe" in s
+    assert "ALU pipe" not in bench.limiter_of(rec, "w10")
     assert bench.limiter_of(dict(rec, dram_throughput_pct=85.0)).startswith("dram-bound")
     assert bench.limiter_of(None) is None
